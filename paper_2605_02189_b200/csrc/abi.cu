@@ -1,0 +1,74 @@
+// C-ABI utilities: version, error strings, TMA descriptor encoding, pinned
+// host memory, batched KV block copies for the offload engine.
+#include <cudaTypedefs.h>
+#include <string.h>
+
+#include "common.cuh"
+
+extern "C" int pm_abi_version(void) { return 1; }
+
+extern "C" const char* pm_error_string(int code) {
+  return cudaGetErrorString(static_cast<cudaError_t>(code));
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major matrix [outer][inner] whose rows are
+// `row_stride_bytes` apart; box = [box_outer][box_inner]; swizzle128 selects
+// the 128-byte swizzle (box_inner*2 must then be 128).  Writes 128 bytes.
+extern "C" int pm_tmap_encode_2d(void* tmap_out, const void* gaddr, unsigned long long inner,
+                                 unsigned long long outer, unsigned long long row_stride_bytes,
+                                 unsigned box_inner, unsigned box_outer, int swizzle128) {
+  auto enc = get_encode();
+  if (!enc) return (int)cudaErrorNotSupported;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(gaddr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
+// Pinned, portable host memory for the KV host replica (the paper's "CPU KV
+// pool").  The caller owns it and frees it with pm_host_free.
+extern "C" int pm_host_alloc(unsigned long long bytes, void** out) {
+  return (int)cudaHostAlloc(out, bytes, cudaHostAllocPortable);
+}
+extern "C" int pm_host_free(void* p) { return (int)cudaFreeHost(p); }
+
+// Batched copies of equal-sized KV pieces between two base addresses:
+// dst_base + dst_off[i] <- src_base + src_off[i], `bytes` each, in order, on
+// `stream` (a copy-engine stream of the offload engine).  Adjacent pieces
+// that are contiguous on both sides are merged into one transfer, so a run
+// of consecutive blocks of one request moves as a single DMA.
+extern "C" int pm_copy_pieces(void* dst_base, const void* src_base, const long long* dst_off,
+                              const long long* src_off, int n, unsigned long long bytes, void* stream) {
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  int i = 0;
+  while (i < n) {
+    int j = i + 1;
+    while (j < n && dst_off[j] == dst_off[j - 1] + (long long)bytes &&
+           src_off[j] == src_off[j - 1] + (long long)bytes)
+      ++j;
+    cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst_base) + dst_off[i],
+                                    static_cast<const char*>(src_base) + src_off[i],
+                                    bytes * (size_t)(j - i), cudaMemcpyDefault, st);
+    if (e != cudaSuccess) return (int)e;
+    i = j;
+  }
+  return 0;
+}

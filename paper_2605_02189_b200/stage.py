@@ -1,0 +1,150 @@
+"""Per-stage decode forward: the layers one pipeline rank owns, their block-
+first KV pool and the kernel sequence of one micro-batch step.
+
+Replaces the reference's simulated ``dur = actual / n`` stage slot
+(REF pipeline_sim.py:423-427, :452-484) with real sm_100a kernels.  Per layer:
+
+  rmsnorm(resid) -> QKV GEMM -> (q/k norm) RoPE + KV append -> paged attention
+  -> O GEMM (+resid, fused epilogue) -> rmsnorm -> gate/up GEMM (SiLU*up fused
+  epilogue) -> down GEMM (+resid, fused epilogue)
+
+The residual stream stays fp32 on the device; GEMM operands are bf16.  All
+buffers are allocated once (``m_cap`` rows) so the step can be captured in a
+CUDA graph and replayed with new metadata.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import ops
+from .models import ModelSpec, init_embed, init_head, init_layer_weights, rope_table
+
+
+def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor:
+    """Rows 2i = gate_i, 2i+1 = up_i so one 128-row GEMM tile holds matching
+    gate/up pairs and the SiLU*up epilogue is a lane-pair shuffle."""
+    return torch.stack([w_gate, w_up], dim=1).reshape(-1, w_gate.shape[1]).contiguous()
+
+
+class StageExecutor:
+    def __init__(self, spec: ModelSpec, layers: range, *, first: bool, last: bool, m_cap: int,
+                 pool_blocks: int, max_blocks: int, n_slots: int, device, seed: int = 0,
+                 max_pos: int = 4096, weights=None, keep_logical=False):
+        self.spec, self.layers = spec, list(layers)
+        self.first, self.last = first, last
+        self.L_s = len(self.layers)
+        self.m_cap, self.max_blocks, self.dev = m_cap, max_blocks, device
+        s = spec
+        self.logical = [] if keep_logical else None
+        self.W = []
+        for li in self.layers:
+            w = weights[li] if weights is not None else init_layer_weights(s, li, device, seed)
+            if keep_logical:
+                self.logical.append(w)
+            qkv = torch.cat([w["wq"], w["wk"], w["wv"]], 0).contiguous()
+            self.W.append(dict(
+                attn_norm=w["attn_norm"], mlp_norm=w["mlp_norm"],
+                q_norm=w.get("q_norm"), k_norm=w.get("k_norm"),
+                qkv=ops.Linear(qkv), o=ops.Linear(w["wo"].contiguous()),
+                gu=ops.Linear(interleave_gate_up(w["w_gate"], w["w_up"])),
+                down=ops.Linear(w["w_down"].contiguous())))
+            if not keep_logical:
+                del w
+        self.embed = init_embed(s, device, seed) if first else None
+        head = init_head(s, device, seed) if last else None
+        self.final_norm = head["final_norm"] if last else None
+        self.lm_head = ops.Linear(head["lm_head"]) if last else None
+        self.rope = torch.from_numpy(rope_table(s, max_pos)).to(device)
+
+        f32, b16, i32 = torch.float32, torch.bfloat16, torch.int32
+        self.resid = torch.zeros(m_cap, s.d, dtype=f32, device=device)
+        self.xn = torch.zeros(m_cap, s.d, dtype=b16, device=device)
+        self.qkv = torch.zeros(m_cap, s.qkv_out, dtype=b16, device=device)
+        self.q = torch.zeros(m_cap, s.H, s.hd, dtype=b16, device=device)
+        self.attn = torch.zeros(m_cap, s.H * s.hd, dtype=b16, device=device)
+        self.act = torch.zeros(m_cap, s.ffn, dtype=b16, device=device)
+        self.xn_maps = ops.activation_maps(self.xn)
+        self.attn_maps = ops.activation_maps(self.attn)
+        self.act_maps = ops.activation_maps(self.act)
+        # KV pool (block-first, token-major inside a block)
+        self.tok_elems = self.L_s * 2 * s.Hkv * s.hd
+        self.tok_bytes = self.tok_elems * 2
+        self.block_bytes = 16 * self.tok_bytes
+        self.pool_blocks = pool_blocks
+        self.pool = torch.zeros(pool_blocks * 16 * self.tok_elems, dtype=b16, device=device)
+        self.pool_map = ops.pool_tmap(self.pool, self.L_s, s.Hkv, s.hd)
+        # per-step metadata (device) and its pinned host staging
+        self.block_table = torch.zeros(m_cap, max_blocks, dtype=i32, device=device)
+        self.positions = torch.zeros(m_cap, dtype=i32, device=device)
+        self.seq_lens = torch.ones(m_cap, dtype=i32, device=device)
+        self.slots = torch.zeros(m_cap, dtype=i32, device=device)
+        self.meta_dev = [self.block_table, self.positions, self.seq_lens, self.slots]
+        self.tok_table = torch.zeros(n_slots, dtype=i32, device=device)
+        self.out_ids = torch.zeros(m_cap, dtype=i32, device=device)
+        self.logits = None
+        # workspaces
+        max_n = max([s.qkv_out, s.d, 2 * s.ffn] + ([s.vocab] if last else []))
+        self.max_splits_attn = max(1, math.ceil(max_blocks / ops.attn_blocks_per_split()))
+        self.gws = ops.GemmWorkspace(m_cap, max(s.qkv_out, s.d, 2 * s.ffn), 16,
+                                     (s.vocab // ops.BM) if last else 1, device)
+        self.ws_o = torch.empty(m_cap * s.H * self.max_splits_attn * s.hd, dtype=f32, device=device)
+        self.ws_ml = torch.empty(m_cap * s.H * self.max_splits_attn * 2, dtype=f32, device=device)
+        self.attn_ctr = torch.zeros(m_cap * s.Hkv, dtype=i32, device=device)
+        del max_n
+
+    # ------------------------------------------------------------------ views
+    def pool_view(self):
+        s = self.spec
+        return self.pool.view(self.pool_blocks, 16, self.L_s, 2, s.Hkv, s.hd)
+
+    def enable_logits(self):
+        if self.last and self.logits is None:
+            self.logits = torch.zeros(self.m_cap, self.spec.vocab, dtype=torch.float32, device=self.dev)
+
+    # ------------------------------------------------------------------ forward
+    def forward(self, M: int, stream=None, kernel_log=None):
+        """One micro-batch step of M rows (metadata already on the device).
+
+        Stage 0 embeds ``tok_table[slots]``; later stages expect ``resid`` to
+        hold the activations received from the previous stage.  The last
+        stage writes greedy ids to ``out_ids`` and ``tok_table[slots]``."""
+        s = self.spec
+        if M == 0:
+            return
+        if self.first:
+            ops.embed(self.tok_table, self.slots, self.embed, self.resid, M, stream)
+        for li, w in enumerate(self.W):
+            ops.rmsnorm(self.resid, w["attn_norm"], self.xn, M, s.eps, stream)
+            w["qkv"](self.xn_maps, M, ops.EPI_STORE_BF16, self.qkv, s.qkv_out, self.gws, stream)
+            ops.qkv_rope_append(self.qkv, self.q, self.pool, self.block_table, self.positions, self.rope,
+                                w["q_norm"], w["k_norm"], M, s.H, s.Hkv, s.hd, li, self.L_s, s.eps, stream)
+            ops.paged_attention(self.pool_map, self.q, self.block_table, self.seq_lens, self.attn, self.ws_o,
+                                self.ws_ml, self.attn_ctr, M, s.H, s.Hkv, s.hd, li, self.L_s,
+                                self.max_splits_attn, stream)
+            w["o"](self.attn_maps, M, ops.EPI_RESID_ADD, self.resid, s.d, self.gws, stream)
+            ops.rmsnorm(self.resid, w["mlp_norm"], self.xn, M, s.eps, stream)
+            w["gu"](self.xn_maps, M, ops.EPI_SILU_MUL, self.act, s.ffn, self.gws, stream)
+            w["down"](self.act_maps, M, ops.EPI_RESID_ADD, self.resid, s.d, self.gws, stream)
+        if self.last:
+            ops.rmsnorm(self.resid, self.final_norm, self.xn, M, s.eps, stream)
+            self.lm_head(self.xn_maps, M, ops.EPI_LOGITS_ARGMAX, self.logits, s.vocab, self.gws, stream)
+            ops.argmax_reduce(self.gws, s.vocab // ops.BM, M, self.out_ids, self.tok_table, self.slots, stream)
+
+    def kernels_per_step(self) -> int:
+        return (1 if self.first else 0) + 8 * self.L_s + (3 if self.last else 0)
+
+    # ------------------------------------------------------------------ roofline
+    def step_bytes(self, M: int, kv_tokens: int) -> int:
+        """Algorithmic HBM bytes of one step: weights once, the micro-batch's
+        KV once per layer, new KV written once, activations (stated, small)."""
+        s = self.spec
+        w = sum(x["qkv"].w.numel() + x["o"].w.numel() + x["gu"].w.numel() + x["down"].w.numel()
+                for x in self.W) * 2
+        if self.last:
+            w += self.lm_head.w.numel() * 2
+        kv = (kv_tokens + M) * self.tok_bytes
+        act = self.L_s * M * (4 * s.d * 4 + 2 * (s.qkv_out + 2 * s.H * s.hd + s.ffn)) * 1
+        return w + kv + act

@@ -1,0 +1,183 @@
+"""Numerics of each sm_100a kernel against plain references (torch fp32 for
+the GEMM, the fp32 numpy oracle for norm / RoPE / paged attention) and
+bit-exact checks of where the KV-append lands in the block-first pool."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import forward_ref as ref
+from paper_2605_02189_b200 import ops
+from paper_2605_02189_b200.models import TINY, QWEN3_8B, rope_table
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def _ws(m_cap, n_out, vocab_tiles=1, splits=16):
+    return ops.GemmWorkspace(m_cap, n_out, splits, vocab_tiles, DEV)
+
+
+@pytest.mark.parametrize("n_out,k,m,splits", [
+    (256, 256, 8, 1), (512, 768, 16, 2), (6144, 4096, 128, 3), (1024, 12288, 64, 4),
+    (384, 1024, 200, 1), (256, 512, 300, 2), (128, 64, 1, 1), (4096, 4096, 32, 5)])
+def test_gemm_store_and_resid(n_out, k, m, splits):
+    g = torch.Generator(device=DEV).manual_seed(n_out + k + m)
+    w = (torch.randn(n_out, k, generator=g, device=DEV) * 0.05).to(torch.bfloat16)
+    m_cap = max(256, m)
+    x = torch.zeros(m_cap, k, device=DEV, dtype=torch.bfloat16)
+    x[:m] = torch.randn(m, k, generator=g, device=DEV).to(torch.bfloat16)
+    lin = ops.Linear(w, splits=splits)
+    maps = ops.activation_maps(x)
+    ws = _ws(m_cap, n_out)
+    want = x[:m].float() @ w.float().T
+    y = torch.zeros(m_cap, n_out, device=DEV, dtype=torch.bfloat16)
+    lin(maps, m, ops.EPI_STORE_BF16, y, n_out, ws)
+    torch.cuda.synchronize()
+    err = (y[:m].float() - want).abs().max().item()
+    assert err <= 2e-2 * max(1.0, want.abs().max().item()), err
+    assert (y[m:] == 0).all()
+    r0 = torch.randn(m_cap, n_out, generator=g, device=DEV)
+    r = r0.clone()
+    lin(maps, m, ops.EPI_RESID_ADD, r, n_out, ws)
+    torch.cuda.synchronize()
+    assert torch.allclose(r[:m], r0[:m] + want, atol=1e-3, rtol=1e-4)
+    assert torch.equal(r[m:], r0[m:])
+    # batch invariance: token 0 alone gives the bit-identical row
+    y1 = torch.zeros_like(y)
+    lin(maps, 1, ops.EPI_STORE_BF16, y1, n_out, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(y1[0], y[0])
+
+
+def test_gemm_silu_mul_interleaved():
+    ffn, k, m = 384, 512, 24
+    g = torch.Generator(device=DEV).manual_seed(3)
+    gate = (torch.randn(ffn, k, generator=g, device=DEV) * 0.05).to(torch.bfloat16)
+    up = (torch.randn(ffn, k, generator=g, device=DEV) * 0.05).to(torch.bfloat16)
+    w = torch.stack([gate, up], dim=1).reshape(2 * ffn, k).contiguous()  # row 2i gate_i, 2i+1 up_i
+    x = torch.zeros(256, k, device=DEV, dtype=torch.bfloat16)
+    x[:m] = torch.randn(m, k, generator=g, device=DEV).to(torch.bfloat16)
+    out = torch.zeros(256, ffn, device=DEV, dtype=torch.bfloat16)
+    ops.Linear(w, splits=2)(ops.activation_maps(x), m, ops.EPI_SILU_MUL, out, ffn, _ws(256, 2 * ffn))
+    torch.cuda.synchronize()
+    gg, uu = x[:m].float() @ gate.float().T, x[:m].float() @ up.float().T
+    want = torch.nn.functional.silu(gg) * uu
+    assert (out[:m].float() - want).abs().max().item() < 2e-2 * want.abs().max().item() + 1e-3
+
+
+@pytest.mark.parametrize("m", [3, 40])
+def test_gemm_logits_argmax(m):
+    V, k = 4096, 256
+    g = torch.Generator(device=DEV).manual_seed(5)
+    w = (torch.randn(V, k, generator=g, device=DEV) * 0.2).to(torch.bfloat16)
+    x = torch.zeros(256, k, device=DEV, dtype=torch.bfloat16)
+    x[:m] = torch.randn(m, k, generator=g, device=DEV).to(torch.bfloat16)
+    ws = _ws(256, V, vocab_tiles=V // 128)
+    logits = torch.zeros(256, V, device=DEV)
+    ops.Linear(w)(ops.activation_maps(x), m, ops.EPI_LOGITS_ARGMAX, logits, V, ws)
+    ids = torch.full((256,), -1, dtype=torch.int32, device=DEV)
+    ops.argmax_reduce(ws, V // 128, m, ids)
+    torch.cuda.synchronize()
+    want = x[:m].float() @ w.float().T
+    assert torch.allclose(logits[:m], want, atol=1e-3, rtol=1e-3)
+    assert torch.equal(ids[:m].long(), logits[:m].argmax(dim=1))
+
+
+def test_rmsnorm_and_embed():
+    d, M = 4096, 37
+    g = torch.Generator(device=DEV).manual_seed(7)
+    table = torch.randn(1000, d, generator=g, device=DEV).to(torch.bfloat16)
+    ids = torch.randint(0, 1000, (M,), generator=g, device=DEV, dtype=torch.int32)
+    resid = torch.empty(M, d, device=DEV)
+    ops.embed(ids, None, table, resid, M)
+    w = (1 + 0.1 * torch.randn(d, generator=g, device=DEV)).to(torch.bfloat16)
+    y = torch.empty(M, d, device=DEV, dtype=torch.bfloat16)
+    ops.rmsnorm(resid, w, y, M, 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(resid, table[ids.long()].float())
+    want = ref.rmsnorm(resid.cpu().numpy(), w.float().cpu().numpy(), 1e-6)
+    np.testing.assert_allclose(y.float().cpu().numpy(), want, atol=2e-2, rtol=1e-2)
+
+
+def _pool(n_blocks, L_s, Hkv, hd):
+    return torch.zeros(n_blocks * 16 * L_s * 2 * Hkv * hd, dtype=torch.bfloat16, device=DEV)
+
+
+@pytest.mark.parametrize("spec", [TINY, QWEN3_8B])
+def test_rope_append_and_paged_attention(spec):
+    """Random prefixes scattered over random physical blocks; the current
+    token goes through the fused qk-norm/RoPE/append kernel, then attention
+    reads the whole prefix through the block table."""
+    rng = np.random.default_rng(11)
+    H, Hkv, hd, L_s, layer = spec.H, spec.Hkv, spec.hd, 3, 1
+    lens = [1, 15, 16, 17, 100, 255, 256, 257, 700, 1025]  # prefix BEFORE this token
+    M = len(lens)
+    max_blocks = 72
+    n_blocks = sum((L + 1 + 15) // 16 for L in lens) + 5
+    perm = rng.permutation(n_blocks)
+    tables = np.zeros((M, max_blocks), np.int32)
+    cur = 0
+    for r, L in enumerate(lens):
+        nb = (L + 1 + 15) // 16
+        tables[r, :nb] = perm[cur:cur + nb]
+        cur += nb
+    pool = _pool(n_blocks, L_s, Hkv, hd)
+    P = pool.view(n_blocks, 16, L_s, 2, Hkv, hd)
+    # existing prefix KV for positions < L (random, written through the table)
+    hist_k = [rng.standard_normal((L, Hkv, hd)).astype(np.float32) for L in lens]
+    hist_v = [rng.standard_normal((L, Hkv, hd)).astype(np.float32) for L in lens]
+    Pc = P.cpu()
+    for r, L in enumerate(lens):
+        for p in range(L):
+            b = tables[r, p // 16]
+            Pc[b, p % 16, layer, 0] = torch.from_numpy(hist_k[r][p]).to(torch.bfloat16)
+            Pc[b, p % 16, layer, 1] = torch.from_numpy(hist_v[r][p]).to(torch.bfloat16)
+    P.copy_(Pc)
+    hist_k = [torch.from_numpy(h).to(torch.bfloat16).float().numpy() for h in hist_k]
+    hist_v = [torch.from_numpy(h).to(torch.bfloat16).float().numpy() for h in hist_v]
+    qkv = torch.from_numpy(rng.standard_normal((M, spec.qkv_out)).astype(np.float32)).to(torch.bfloat16).to(DEV)
+    rope = torch.from_numpy(rope_table(spec, 2048)).to(DEV)
+    qn = kn = None
+    if spec.qk_norm:
+        qn = (1 + 0.1 * torch.randn(hd, device=DEV)).to(torch.bfloat16)
+        kn = (1 + 0.1 * torch.randn(hd, device=DEV)).to(torch.bfloat16)
+    q_out = torch.empty(M, H, hd, dtype=torch.bfloat16, device=DEV)
+    bt = torch.from_numpy(tables).to(DEV)
+    pos = torch.tensor(lens, dtype=torch.int32, device=DEV)
+    ops.qkv_rope_append(qkv, q_out, pool, bt, pos, rope, qn, kn, M, H, Hkv, hd, layer, L_s, spec.eps)
+    bps = ops.attn_blocks_per_split()
+    max_splits = math.ceil(max_blocks / bps)
+    ws_o = torch.empty(M * H * max_splits * hd, device=DEV)
+    ws_ml = torch.empty(M * H * max_splits * 2, device=DEV)
+    ctr = torch.zeros(M * Hkv, dtype=torch.int32, device=DEV)
+    out = torch.empty(M, H, hd, dtype=torch.bfloat16, device=DEV)
+    seq = pos + 1
+    tmap = ops.pool_tmap(pool, L_s, Hkv, hd)
+    ops.paged_attention(tmap, q_out, bt, seq, out, ws_o, ws_ml, ctr, M, H, Hkv, hd, layer, L_s, max_splits)
+    torch.cuda.synchronize()
+    assert (ctr == 0).all()
+    tab = rope_table(spec, 2048)
+    x = qkv.float().cpu().numpy()
+    Pn = P.float().cpu().numpy()
+    for r, L in enumerate(lens):
+        q = x[r, :H * hd].reshape(H, hd)
+        k = x[r, H * hd:(H + Hkv) * hd].reshape(Hkv, hd)
+        v = x[r, (H + Hkv) * hd:].reshape(Hkv, hd)
+        if spec.qk_norm:
+            q = ref.rmsnorm(q, qn.float().cpu().numpy(), spec.eps)
+            k = ref.rmsnorm(k, kn.float().cpu().numpy(), spec.eps)
+        q, k = ref.rope(q, L, tab), ref.rope(k, L, tab)
+        np.testing.assert_allclose(q_out[r].float().cpu().numpy(), q, atol=3e-2, rtol=1e-2)
+        b, s = tables[r, L // 16], L % 16
+        np.testing.assert_allclose(Pn[b, s, layer, 0], k, atol=3e-2, rtol=1e-2)
+        assert np.array_equal(Pn[b, s, layer, 1], torch.from_numpy(v).to(torch.bfloat16).float().numpy())
+        # attention uses the bf16 values actually stored / produced
+        K = np.concatenate([hist_k[r], Pn[b, s, layer, 0][None]], 0)
+        V = np.concatenate([hist_v[r], Pn[b, s, layer, 1][None]], 0)
+        want = ref.attend(q_out[r].float().cpu().numpy(), K, V, H // Hkv)
+        got = out[r].float().cpu().numpy()
+        np.testing.assert_allclose(got, want, atol=2e-2, rtol=2e-2, err_msg=f"row {r} len {L}")
+    # untouched layers / slots stay zero
+    assert np.all(Pn[:, :, 0] == 0) and np.all(Pn[:, :, 2] == 0)
