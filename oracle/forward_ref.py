@@ -35,6 +35,13 @@ def rope(x, pos, table):
     return np.concatenate([x1 * cos - x2 * sin, x2 * cos + x1 * sin], axis=-1)
 
 
+def bf16(x):
+    """Round fp32 -> bf16 (round-to-nearest-even) and back, in numpy."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32)
+
+
 def silu(x):
     return x / (1.0 + np.exp(-x))
 
@@ -55,7 +62,12 @@ class RefModel:
     """hp: dict(d, layers, H, Hkv, hd, ffn, vocab, qk_norm, eps); layers: list
     of dicts of fp32 arrays (HF layout [out, in]); embed, final_norm, lm_head."""
 
-    def __init__(self, hp, layers, embed, final_norm, lm_head, rope_tab):
+    def __init__(self, hp, layers, embed, final_norm, lm_head, rope_tab, storage_bf16=False):
+        """storage_bf16: also round to bf16 wherever the GPU path STORES a bf16
+        tensor (norm outputs, qkv, q, cached k/v, attention output, SwiGLU
+        activation) -- a diagnostic twin that isolates kernel arithmetic from
+        bf16 storage error.  The default is the pure fp32 reference."""
+        self.r = bf16 if storage_bf16 else (lambda x: x)
         self.hp = hp
         self.layers = layers
         self.embed = embed
@@ -70,28 +82,29 @@ class RefModel:
         """One token of one request through layer li; x [d] fp32; cache list of (K, V)."""
         hp, w = self.hp, self.layers[li]
         H, Hkv, hd, eps = hp["H"], hp["Hkv"], hp["hd"], hp["eps"]
-        h = rmsnorm(x, w["attn_norm"], eps)
-        q = (w["wq"] @ h).reshape(H, hd)
-        k = (w["wk"] @ h).reshape(Hkv, hd)
-        v = (w["wv"] @ h).reshape(Hkv, hd)
+        R = self.r
+        h = R(rmsnorm(x, w["attn_norm"], eps))
+        q = R(w["wq"] @ h).reshape(H, hd)
+        k = R(w["wk"] @ h).reshape(Hkv, hd)
+        v = R(w["wv"] @ h).reshape(Hkv, hd)
         if hp["qk_norm"]:
             q = rmsnorm(q, w["q_norm"], eps)
             k = rmsnorm(k, w["k_norm"], eps)
-        q = rope(q, pos, self.rope)
-        k = rope(k, pos, self.rope)
+        q = R(rope(q, pos, self.rope))
+        k = R(rope(k, pos, self.rope))
         cache[0].append(k)
         cache[1].append(v)
-        o = attend(q, np.stack(cache[0]), np.stack(cache[1]), H // Hkv)
+        o = R(attend(q, np.stack(cache[0]), np.stack(cache[1]), H // Hkv))
         x = x + w["wo"] @ o.reshape(-1)
-        h = rmsnorm(x, w["mlp_norm"], eps)
-        return x + w["w_down"] @ (silu(w["w_gate"] @ h) * (w["w_up"] @ h))
+        h = R(rmsnorm(x, w["mlp_norm"], eps))
+        return x + w["w_down"] @ R(silu(w["w_gate"] @ h) * (w["w_up"] @ h))
 
     def token_step(self, tok, pos, caches):
         """Embed one token at position pos, run all layers; returns logits [V]."""
         x = self.embed[tok].astype(np.float32)
         for li in range(len(self.layers)):
             x = self.layer_step(li, x, pos, caches[li])
-        return self.lm_head @ rmsnorm(x, self.final_norm, self.hp["eps"])
+        return self.lm_head @ self.r(rmsnorm(x, self.final_norm, self.hp["eps"]))
 
     def run_request(self, prompt, n_gen, forced=None):
         """Teacher-force the prompt, then decode n_gen tokens.  If ``forced``

@@ -1,0 +1,296 @@
+"""The B200 decode engine: the reference's ``simulate_decode`` driver shape
+over real hardware.
+
+``run_decode(state, cfg, params, spec, requests=..., horizon=...)`` mirrors
+``pipemax.pipeline_sim.simulate_decode`` (REF pkg/src/pipemax/
+pipeline_sim.py:546-581) and returns ``(EventTrace, EpisodeMetrics)``; the
+loop body is the reference's ``_DecodeEngine.run`` (:386-543) with the
+simulated pieces replaced:
+
+  reference                                  B200
+  ---------                                  ----
+  _plan_step / commit / GpuState counts      DecodeControl (same code path, run
+                                             ahead of the GPU) + physical blocks
+  estimate_decode_time x noise / n           StageExecutor.forward (sm_100a)
+  h2d.submit_stream(kv_prefetch)             KvEngine.prefetch  (H2D copy stream)
+  h2d.finish_stream -> stall                 compute-stream wait on the H2D event
+  d2h.submit_stream(kv_offload_decode)       KvEngine.offload   (D2H copy stream)
+  submit_high activation hop                 NCCL send/recv between stage ranks
+
+With ``pp > 1`` in one process (``local_pipeline=True``) the stages run back
+to back on one device -- used by tests to validate the layer split; the
+multi-GPU path (one rank per stage) lives in ``pipeline.py``.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from .control import DecodeControl, StepWork
+from .kv import HostReplica, KvEngine
+from .model_core import ClusterConfig, EstimatorParams, blocks_for_tokens
+from .models import ModelSpec, stage_layers
+from .scheduler import SchedulerState
+from .stage import StageExecutor
+from .trace import EpisodeMetrics, EventTrace
+
+
+class _MetaRing:
+    """Pinned host staging for per-step metadata; ``depth`` buffers so the
+    host can run ahead of the GPU without overwriting an in-flight copy."""
+
+    def __init__(self, m_cap, max_blocks, depth=4):
+        self.bufs = [torch.zeros(m_cap * (max_blocks + 3), dtype=torch.int32).pin_memory() for _ in range(depth)]
+        self.events = [None] * depth
+        self.i = 0
+        self.m_cap, self.max_blocks = m_cap, max_blocks
+
+    def next(self):
+        k = self.i % len(self.bufs)
+        self.i += 1
+        for ev in self.events[k] or ():
+            ev.synchronize()
+        return k, self.bufs[k]
+
+
+class DecodeEngine:
+    def __init__(self, spec: ModelSpec, state: SchedulerState, cfg: ClusterConfig, params: EstimatorParams,
+                 requests: dict, *, pp: int = 1, device="cuda", mode="dynamic", quota_tokens=0,
+                 seed: int = 0, m_cap: int = None, timing=True, kv_init="random", prompts=None,
+                 record_logits=False, max_pos=None, trace: EventTrace = None):
+        self.spec, self.cfg, self.params = spec, cfg, params
+        self.requests = requests
+        self.dev = torch.device(device)
+        self.metrics = EpisodeMetrics()
+        self.trace = trace if trace is not None else EventTrace()
+        self.control = DecodeControl(state, cfg, params, requests, mode=mode, quota_tokens=quota_tokens,
+                                     metrics=self.metrics)
+        bs = cfg.block_size
+        assert bs == 16, "the kernels use 16-token blocks"
+        rids = sorted(requests)
+        self.slot_of = {rid: i for i, rid in enumerate(rids)}
+        max_len = max(r.input_len + r.output_len for r in requests.values())
+        self.max_blocks = blocks_for_tokens(max_len + 1, bs)
+        self.m_cap = m_cap or len(rids)
+        self.max_pos = max_pos or (self.max_blocks * bs)
+        pool_blocks = self.control.alloc.total
+        self.stages = []
+        for s in range(pp):
+            ex = StageExecutor(spec, stage_layers(spec, pp, s), first=(s == 0), last=(s == pp - 1),
+                               m_cap=self.m_cap, pool_blocks=pool_blocks, max_blocks=self.max_blocks,
+                               n_slots=len(rids), device=self.dev, seed=seed, max_pos=self.max_pos,
+                               keep_logical=record_logits)
+            if record_logits:
+                ex.enable_logits()
+            rep = HostReplica(len(rids), self.max_blocks, ex.block_bytes)
+            self.stages.append((ex, KvEngine(ex, rep, self.slot_of, self.dev, timing=timing)))
+        self.meta = _MetaRing(self.m_cap, self.max_blocks)
+        self.record_logits = record_logits
+        self.logits_log = []   # (t, rows, positions, logits[M, V] np) when recording
+        self.ids_log = []      # (t, rows, ids np)
+        self.t = 0
+        self.n_evicted = self.n_prefetched = 0
+        self._init_kv(kv_init, prompts, seed)
+
+    # ------------------------------------------------------------------ setup
+    def _init_kv(self, how, prompts, seed):
+        """Seed every request's KV: the host replica holds all of it, the
+        resident requests' blocks also sit in HBM (REF run_episode's initial
+        bulk load, pipeline_sim.py:732-739)."""
+        rids = sorted(self.requests)
+        g = torch.Generator(device=self.dev).manual_seed(seed + 1)
+        first_tok = torch.randint(0, self.spec.vocab, (len(rids),), generator=g, device=self.dev,
+                                  dtype=torch.int32)
+        for ex, kv in self.stages:
+            if ex.first:
+                ex.tok_table.copy_(first_tok)
+        torch.cuda.synchronize()
+        if how == "prefill":
+            assert prompts is not None
+            self._prefill(prompts)
+            return
+        # timing runs: random KV in HBM for resident blocks; the host replica
+        # keeps whatever the fresh pinned pages hold (zeros) -- values do not
+        # change the timing
+        for ex, kv in self.stages:
+            pv = ex.pool.view(ex.pool_blocks, -1)
+            for rid, blocks in self.control.alloc.tables.items():
+                idx = torch.tensor(blocks, device=self.dev)
+                pv[idx] = (torch.randn(len(blocks), pv.shape[1], generator=g, device=self.dev) * 0.5).to(torch.bfloat16)
+        torch.cuda.synchronize()
+
+    def _prefill(self, prompts):
+        """Prefill by teacher-forced decode steps through the same kernels
+        (SURVEY.md 8f row 1 is the real prefill path; this seeds parity runs).
+        Each request's prompt KV is written to scratch blocks, copied to its
+        host replica region, and resident requests' blocks are then filled
+        from the host copy like any prefetch."""
+        rids = sorted(self.requests)
+        free = sorted(set(range(self.control.alloc.total)) -
+                      {b for t in self.control.alloc.tables.values() for b in t})
+        # groups of requests that fit the scratch blocks and m_cap rows
+        groups, cur, used = [], [], 0
+        for rid in rids:
+            need = blocks_for_tokens(len(prompts[rid]), 16)
+            if cur and (used + need > len(free) or len(cur) >= self.m_cap):
+                groups.append(cur)
+                cur, used = [], 0
+            cur.append(rid)
+            used += need
+        if cur:
+            groups.append(cur)
+        for group in groups:
+            tables, k = {}, 0
+            for rid in group:
+                need = blocks_for_tokens(len(prompts[rid]), 16)
+                tables[rid] = free[k:k + need]
+                k += need
+            P = max(len(prompts[r]) for r in group)
+            for p in range(P):
+                rows = [r for r in group if p < len(prompts[r])]
+                ex0, kv0 = self.stages[0]
+                with torch.cuda.stream(kv0.compute):
+                    tok = torch.tensor([int(prompts[r][p]) for r in rows], dtype=torch.int32)
+                    idx = torch.tensor([self.slot_of[r] for r in rows])
+                    ex0.tok_table[idx.to(self.dev)] = tok.to(self.dev)
+                self._upload_meta(rows, [p] * len(rows), tables)
+                self._forward_all(len(rows))
+            torch.cuda.synchronize()
+            for ex, kv in self.stages:
+                host = kv.rep.as_tensor()
+                pv = ex.pool.view(torch.uint8).view(ex.pool_blocks, ex.block_bytes)
+                for rid in group:
+                    off = kv.rep.offset(self.slot_of[rid])
+                    for lb, pb in enumerate(tables[rid]):
+                        host[off + lb * ex.block_bytes: off + (lb + 1) * ex.block_bytes].copy_(pv[pb].cpu())
+        # first generated token came out of the last prompt step; move it to stage 0
+        if len(self.stages) > 1:
+            self.stages[0][0].tok_table.copy_(self.stages[-1][0].tok_table)
+        for ex, kv in self.stages:
+            host = kv.rep.as_tensor()
+            pv = ex.pool.view(torch.uint8).view(ex.pool_blocks, ex.block_bytes)
+            for rid, blocks in self.control.alloc.tables.items():
+                off = kv.rep.offset(self.slot_of[rid])
+                for lb, pb in enumerate(blocks):
+                    pv[pb].copy_(host[off + lb * ex.block_bytes: off + (lb + 1) * ex.block_bytes].to(self.dev))
+        torch.cuda.synchronize()
+
+    # ------------------------------------------------------------------ per step
+    def _upload_meta(self, rows, positions, tables, stream=None):
+        M, mb = len(rows), self.max_blocks
+        k, buf = self.meta.next()
+        a = buf.numpy()
+        bt = a[:M * mb].reshape(M, mb)
+        bt[:] = 0
+        for i, r in enumerate(rows):
+            tb = tables[r]
+            bt[i, :len(tb)] = tb
+        o = M * mb
+        a[o:o + M] = positions
+        a[o + M:o + 2 * M] = np.asarray(positions) + 1
+        a[o + 2 * M:o + 3 * M] = [self.slot_of[r] for r in rows]
+        evs = []
+        for ex, kv in self.stages:
+            s = kv.compute if stream is None else stream
+            with torch.cuda.stream(s):
+                ex.block_table[:M].view(-1).copy_(buf[:M * mb], non_blocking=True)
+                ex.positions[:M].copy_(buf[o:o + M], non_blocking=True)
+                ex.seq_lens[:M].copy_(buf[o + M:o + 2 * M], non_blocking=True)
+                ex.slots[:M].copy_(buf[o + 2 * M:o + 3 * M], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(s)
+            evs.append(ev)
+        self.meta.events[k] = evs
+
+    def _forward_all(self, M):
+        """Run the stages in order on their compute streams (single process:
+        stage s+1 waits for stage s's activations via an event)."""
+        prev_ev = None
+        for si, (ex, kv) in enumerate(self.stages):
+            if prev_ev is not None:
+                kv.compute.wait_event(prev_ev)
+            with torch.cuda.stream(kv.compute):
+                if si > 0:
+                    ex.resid[:M].copy_(self.stages[si - 1][0].resid[:M])
+                ex.forward(M, kv.compute)
+                if si == len(self.stages) - 1 and len(self.stages) > 1:
+                    # greedy ids back to stage 0's token table (the last->first hop)
+                    first = self.stages[0][0]
+                    first.tok_table.copy_(ex.tok_table)
+            prev_ev = torch.cuda.Event()
+            prev_ev.record(kv.compute)
+        if len(self.stages) > 1:
+            self.stages[0][1].compute.wait_event(prev_ev)
+
+    def step(self) -> StepWork:
+        work = self.control.step()
+        if work is None:
+            return None
+        t = self.t
+        M = len(work.rows)
+        self.n_evicted += len(work.evicted) + len(work.relief_evicted)
+        self.n_prefetched += len(work.prefetch)
+        recs = []
+        for ex, kv in self.stages:
+            rec = {"t": t, "M": M}
+            kv.prefetch(t, work, rec)
+            recs.append(rec)
+        self._upload_meta(work.rows, work.positions, work.tables)
+        for (ex, kv), rec in zip(self.stages, recs):
+            kv.before_compute(t, work, rec)
+        self._forward_all(M)
+        for (ex, kv), rec in zip(self.stages, recs):
+            kv.after_compute(t, rec)
+            kv.offload(t, work, rec)
+        if self.record_logits and M:
+            last = self.stages[-1][0]
+            torch.cuda.synchronize()
+            self.logits_log.append((t, list(work.rows), list(work.positions), last.logits[:M].cpu().numpy()))
+            self.ids_log.append((t, list(work.rows), last.out_ids[:M].cpu().numpy().copy()))
+        self.t += 1
+        return work
+
+    def run(self, horizon=None):
+        n = 0
+        while horizon is None or n < horizon:
+            if self.step() is None:
+                break
+            n += 1
+        torch.cuda.synchronize()
+        return n
+
+    def finalize_metrics(self, wall_seconds: float):
+        m = self.metrics
+        stall = h2d = d2h = 0.0
+        for ex, kv in self.stages:
+            s, a, b, _ = kv.timings()
+            stall, h2d, d2h = max(stall, s), max(h2d, a), max(d2h, b)
+        m.stall_seconds = stall
+        m.h2d_busy_seconds, m.d2h_busy_seconds = h2d, d2h
+        m.h2d_bytes = sum(kv.h2d_bytes for _, kv in self.stages)
+        m.d2h_bytes = sum(kv.d2h_bytes for _, kv in self.stages)
+        m.wall_seconds = m.decode_seconds = wall_seconds
+        return m.finalize()
+
+
+def run_decode(state: SchedulerState, cfg: ClusterConfig, params: EstimatorParams, spec: ModelSpec,
+               noise_spec=None, horizon: int = None, *, requests: dict, seed: int = 0, pp: int = 1,
+               device="cuda", kv_init="random", prompts=None, **kw):
+    """Drop-in for ``simulate_decode`` (REF pipeline_sim.py:546-581) on B200:
+    same positional/keyword shape plus the model spec; ``noise_spec`` is
+    accepted and ignored (durations are measured).  Returns (trace, metrics)."""
+    eng = DecodeEngine(spec, state, cfg, params, requests, pp=pp, device=device, seed=seed,
+                       kv_init=kv_init, prompts=prompts, **kw)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record()
+    eng.run(horizon)
+    end.record()
+    torch.cuda.synchronize()
+    wall = start.elapsed_time(end) * 1e-3
+    m = eng.finalize_metrics(wall)
+    eng.trace.finalize()
+    return eng.trace, m

@@ -1,0 +1,205 @@
+"""KV offload engine of one pipeline stage: pinned host replica + copy-engine
+streams, event-ordered against the compute stream.
+
+Replaces the reference's simulated links (REF = reference
+``pkg/src/pipemax``): ``ChannelSim.submit_stream`` prefetch (pipeline_sim.py
+:442-450, transfer.py:237-257), the eager decode offload (pipeline_sim.py
+:486-490) and ``GpuState`` residency (:121-153).
+
+* Host replica: one contiguous, block-first region per request slot
+  ``[max_blocks][16][L_s][2][Hkv][hd]`` bf16 in pinned memory.  It is kept
+  complete (every new token is offloaded the step it is produced), so an
+  eviction costs no copy -- exactly the reference's invariant
+  (scheduler.py:318-321).
+* Prefetch (plan t): whole blocks host->HBM on the H2D stream, one DMA per
+  run of consecutive physical blocks.  Ordered after the compute step that
+  last read the reused blocks and after the offload that last wrote the
+  prefetched requests' host copy; the step that first executes them waits on
+  it (the stall the reference models at pipeline_sim.py:410-421).
+* Offload (step t): the new token's whole-stage KV (one contiguous slot per
+  row) HBM->host on the D2H stream right after the step's compute.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _C
+
+
+class HostReplica:
+    """Pinned host KV: ``slots`` request regions of ``max_blocks`` blocks."""
+
+    def __init__(self, slots: int, max_blocks: int, block_bytes: int):
+        self.slots, self.max_blocks, self.block_bytes = slots, max_blocks, block_bytes
+        self.region_bytes = max_blocks * block_bytes
+        self.nbytes = slots * self.region_bytes
+        ptr = _C.C.c_void_p()
+        _C.call("pm_host_alloc", self.nbytes, _C.C.byref(ptr))
+        self.ptr = ptr.value
+
+    def offset(self, slot: int, block: int = 0) -> int:
+        return slot * self.region_bytes + block * self.block_bytes
+
+    def as_tensor(self):
+        """uint8 view (tests / prefill seeding)."""
+        import ctypes
+        buf = (ctypes.c_uint8 * self.nbytes).from_address(self.ptr)
+        return torch.frombuffer(buf, dtype=torch.uint8)
+
+    def close(self):
+        if self.ptr:
+            _C.call("pm_host_free", _C.C.c_void_p(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class KvEngine:
+    """Copy streams, events and the dependency rules of one stage."""
+
+    def __init__(self, executor, replica: HostReplica, slot_of: dict, device, timing: bool = True):
+        self.ex, self.rep, self.slot_of = executor, replica, slot_of
+        self.dev = device
+        lo, hi = torch.cuda.Stream.priority_range()
+        self.compute = torch.cuda.Stream(device=device, priority=hi)
+        self.h2d = torch.cuda.Stream(device=device, priority=lo)
+        self.d2h = torch.cuda.Stream(device=device, priority=lo)
+        self.timing = timing
+        self.pool_ptr = executor.pool.data_ptr()
+        self.block_bytes = executor.block_bytes
+        self.tok_bytes = executor.tok_bytes
+        self.last_write = {}        # rid -> step whose offload last wrote its host copy
+        self.d2h_done = {}          # step -> event
+        self.compute_done = {}      # step -> event
+        self.h2d_done = {}          # step -> event (plan t's prefetch)
+        self.records = []           # per step timing events
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+        self.block_last_d2h = np.full(executor.pool_blocks, -1, dtype=np.int64)
+
+    def _event(self):
+        return torch.cuda.Event(enable_timing=self.timing)
+
+    # -- H2D prefetch of plan t ---------------------------------------------------
+    def prefetch(self, t: int, work, rec: dict):
+        """Issue plan t's host->HBM block copies (REF pipeline_sim.py:442-450)."""
+        self.records.append(rec)
+        if not work.prefetch:
+            self.h2d_done[t] = None
+            return
+        bb = self.block_bytes
+        dst, src, targets = [], [], set()
+        for rid, blocks, _n in work.prefetch:
+            base = self.rep.offset(self.slot_of[rid])
+            for lb, pb in enumerate(blocks):
+                dst.append(pb * bb)
+                src.append(base + lb * bb)
+                targets.add(pb)
+        s = self.h2d
+        prev = self.compute_done.get(t - 1)
+        if prev is not None:
+            s.wait_event(prev)            # reused blocks were last read by step t-1
+        # the host copy must hold the requests' last token, and no offload may
+        # still be reading a block this copy overwrites
+        dep = max((self.last_write.get(rid, -1) for rid, _, _ in work.prefetch), default=-1)
+        dep = max(dep, int(self.block_last_d2h[list(targets)].max()))
+        ev = self.d2h_done.get(dep)
+        if ev is not None:
+            s.wait_event(ev)
+        with torch.cuda.stream(s):
+            if self.timing:
+                rec["h2d_start"] = self._event()
+                rec["h2d_start"].record(s)
+            n = len(dst)
+            d = np.asarray(dst, dtype=np.int64)
+            sr = np.asarray(src, dtype=np.int64)
+            _C.call("pm_copy_pieces", _C.C.c_void_p(self.pool_ptr), _C.C.c_void_p(self.rep.ptr),
+                    d.ctypes.data_as(_C.C.c_void_p), sr.ctypes.data_as(_C.C.c_void_p), n, bb,
+                    _C.C.c_void_p(s.cuda_stream))
+            done = self._event()
+            done.record(s)
+        rec["h2d_end"] = done
+        rec["h2d_bytes"] = len(dst) * bb
+        self.h2d_bytes += len(dst) * bb
+        self.h2d_done[t] = done
+
+    # -- compute ordering -----------------------------------------------------------
+    def before_compute(self, t: int, work, rec: dict):
+        s = self.compute
+        if self.timing:
+            rec["ready"] = self._event()
+            rec["ready"].record(s)
+        ev = self.h2d_done.get(t - 1)
+        if ev is not None:
+            s.wait_event(ev)              # batch i's newest members arrived with plan t-1
+        # a growth block handed out this step may still be read by an offload
+        grow = [work.tables[r][p // 16] for r, p in zip(work.rows, work.positions) if p % 16 == 0]
+        if grow:
+            dep = int(self.block_last_d2h[grow].max())
+            ev = self.d2h_done.get(dep)
+            if ev is not None:
+                s.wait_event(ev)
+        if self.timing:
+            rec["start"] = self._event()
+            rec["start"].record(s)
+
+    def after_compute(self, t: int, rec: dict):
+        done = self._event()
+        done.record(self.compute)
+        rec["end"] = done
+        self.compute_done[t] = done
+
+    # -- D2H offload of step t --------------------------------------------------------
+    def offload(self, t: int, work, rec: dict):
+        """Eager offload of the step's new KV (REF pipeline_sim.py:486-490)."""
+        rows = work.offload_rows
+        if not rows:
+            self.d2h_done[t] = None
+            return
+        tb, bb = self.tok_bytes, self.block_bytes
+        src, dst = [], []
+        for ix in rows:
+            rid, pos = work.rows[ix], work.positions[ix]
+            blk = work.tables[rid][pos // 16]
+            src.append(blk * bb + (pos % 16) * tb)
+            dst.append(self.rep.offset(self.slot_of[rid]) + pos * tb)
+            self.last_write[rid] = t
+            self.block_last_d2h[blk] = t
+        s = self.d2h
+        s.wait_event(self.compute_done[t])
+        with torch.cuda.stream(s):
+            if self.timing:
+                rec["d2h_start"] = self._event()
+                rec["d2h_start"].record(s)
+            d = np.asarray(dst, dtype=np.int64)
+            sr = np.asarray(src, dtype=np.int64)
+            _C.call("pm_copy_pieces", _C.C.c_void_p(self.rep.ptr), _C.C.c_void_p(self.pool_ptr),
+                    d.ctypes.data_as(_C.C.c_void_p), sr.ctypes.data_as(_C.C.c_void_p), len(rows), tb,
+                    _C.C.c_void_p(s.cuda_stream))
+            done = self._event()
+            done.record(s)
+        rec["d2h_end"] = done
+        rec["d2h_bytes"] = len(rows) * tb
+        self.d2h_bytes += len(rows) * tb
+        self.d2h_done[t] = done
+
+    # -- accounting ---------------------------------------------------------------------
+    def timings(self):
+        """(stall_s, h2d_busy_s, d2h_busy_s, compute_s) from the recorded events."""
+        stall = h2d = d2h = comp = 0.0
+        for rec in self.records:
+            if "ready" in rec and "start" in rec:
+                stall += rec["ready"].elapsed_time(rec["start"]) * 1e-3
+            if "h2d_start" in rec:
+                h2d += rec["h2d_start"].elapsed_time(rec["h2d_end"]) * 1e-3
+            if "d2h_start" in rec:
+                d2h += rec["d2h_start"].elapsed_time(rec["d2h_end"]) * 1e-3
+            if "start" in rec and "end" in rec:
+                comp += rec["start"].elapsed_time(rec["end"]) * 1e-3
+        return stall, h2d, d2h, comp

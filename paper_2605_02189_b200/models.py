@@ -51,7 +51,7 @@ class ModelSpec:
 
 
 # tiny: builder's choice recorded in DESIGN.md (H=4, Hkv=2, hd=64, ffn=768, V=4096)
-TINY = ModelSpec("tiny-llama", 256, 4, 4, 2, 64, 768, 4096, False, 10000.0, 1e-5, lm_head_std=0.2)
+TINY = ModelSpec("tiny-llama", 256, 4, 4, 2, 64, 768, 4096, False, 10000.0, 1e-5)
 QWEN3_8B = ModelSpec("qwen3-8b", 4096, 36, 32, 8, 128, 12288, 151936, True, 1e6, 1e-6)
 QWEN3_32B = ModelSpec("qwen3-32b", 5120, 64, 64, 8, 128, 25600, 151936, True, 1e6, 1e-6)
 LLAMA3_70B = ModelSpec("llama3-70b", 8192, 80, 64, 8, 128, 28672, 128256, False, 5e5, 1e-5)
