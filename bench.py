@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Decode throughput of the B200 PipeMax decode path (one JSON line).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (N=1): BASELINE.json configs[1] -- Qwen3-8B shape (36 layers,
+d=4096, GQA 32/8, hd=128, ffn 12288, V=151936, random init, bf16), 256
+requests, prompt 512 / gen 512, 2 cyclic micro-batches (~128 rows each),
+block-first KV pool capped at 75% of the batch's peak KV so the scheduler
+offloads/prefetches through pinned host memory.  On one GPU the pipeline is
+PP=1 (every layer on the GPU); with N>1 under torchrun each rank runs an
+independent replica of the same workload (replicas; the PP path is
+``pipeline.py``).  A "step" is one rotation iteration of the reference engine
+(REF pipeline_sim.py:386-543): plan + prefetch + one micro-batch through all
+layers + offload.  Inputs > L2 (weights 16 GB, KV > 10 GB per step).
+
+The reference arm (``--impl reference``) times the CPU implementation of the
+path -- the fp32 numpy oracle port of the same decode step (the reference
+itself has no model math) -- on all host threads, on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p, "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+# ---------------------------------------------------------------- workload
+def workload(spec_name="qwen3-8b", n_req=256, prompt=512, gen=512, m=2, cap_frac=0.75, resident_frac=0.75,
+             seed=0):
+    from paper_2605_02189_b200 import scheduler as sched
+    from paper_2605_02189_b200.model_core import ClusterConfig, EstimatorParams, Request
+    from paper_2605_02189_b200.models import SPECS
+
+    spec = SPECS[spec_name]
+    kv_tok = spec.kv_bytes_per_token()
+    reqs = {i: Request(i, prompt, gen) for i in range(n_req)}
+    peak_blocks = n_req * math.ceil((prompt + gen) / 16)
+    cap = int(peak_blocks * cap_frac)
+    # 75% of the batch starts in HBM; the rest waits in the pinned host pool
+    # and is prefetched by the scheduler as the budget and free blocks allow
+    resident = list(range(int(n_req * resident_frac)))
+    batches = sched.initial_partition([reqs[r] for r in resident], m)
+    state = sched.SchedulerState(n=m, batches=batches, lengths={r: q.prefix_len for r, q in reqs.items()},
+                                 gpu_resident=set(resident), cpu_pool=set(reqs) - set(resident),
+                                 ema_alpha=0.3)
+    mem = -(-cap * 16 * kv_tok // m)
+    cfg = ClusterConfig(n=m, mem_per_gpu=mem, model_bytes=0, kv_bytes_per_token=kv_tok,
+                        h2d_bandwidth=55e9, d2h_bandwidth=55e9, cpu_kv_capacity=10**15, block_size=16)
+    hbm = 6.5459e12
+    # B200 estimator: linears weight-bound (alpha~0), attention KV-bound
+    params = EstimatorParams(1e-7, kv_tok / hbm, spec.weight_bytes() / hbm)
+    desc = {"workload": f"{spec_name} decode, PP=1, {m} micro-batches, bs {n_req}, prompt {prompt} / gen {gen}, "
+                        f"KV pool capped at {cap_frac:.0%} of peak, {1 - resident_frac:.0%} of requests start in host memory "
+                        f"(offload on)",
+            "model": spec_name, "global_batch": n_req, "seq_len": prompt + gen, "micro_batches": m,
+            "pool_blocks": cap, "parallelism": "pp1", "l2": "inputs > L2 (weights + KV per step >> 126 MB)"}
+    return spec, state, cfg, params, reqs, desc
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, gpu=0):
+        self.samples, self.stop = [], threading.Event()
+        self.gpu = gpu
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for i, n in enumerate(names):
+                if len(s) > 3 + i and "Active" in s[3 + i] and "Not" not in s[3 + i]:
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- CPU leg
+def cpu_port_step_seconds(spec, M, ctx, layers_sample=1, seed=0):
+    """Time the fp32 numpy oracle port of one decode step on a bounded
+    sample: ``layers_sample`` full decoder layers for M rows at context
+    ``ctx`` (attention per request, unbatched KV), plus lm_head; scaled to the
+    whole model.  Returns (seconds per step, threads, sample description)."""
+    import numpy as np
+    from oracle import forward_ref as ref
+    rng = np.random.default_rng(seed)
+    d, H, Hkv, hd, f = spec.d, spec.H, spec.Hkv, spec.hd, spec.ffn
+    W = lambda *s: (rng.standard_normal(s, dtype=np.float32) * 0.02)
+    wq, wk, wv, wo = W(H * hd, d), W(Hkv * hd, d), W(Hkv * hd, d), W(d, H * hd)
+    wg, wu, wd = W(f, d), W(f, d), W(d, f)
+    x = rng.standard_normal((M, d), dtype=np.float32)
+    K = rng.standard_normal((ctx, Hkv, hd), dtype=np.float32)
+    V = rng.standard_normal((ctx, Hkv, hd), dtype=np.float32)
+    nw = np.ones(d, np.float32)
+    t0 = time.perf_counter()
+    for _ in range(layers_sample):
+        h = ref.rmsnorm(x, nw, spec.eps)
+        q = (h @ wq.T).reshape(M, H, hd)
+        _ = h @ wk.T, h @ wv.T
+        o = np.stack([ref.attend(q[r], K, V, H // Hkv) for r in range(M)])
+        x = x + o.reshape(M, -1) @ wo.T
+        h = ref.rmsnorm(x, nw, spec.eps)
+        x = x + (ref.silu(h @ wg.T) * (h @ wu.T)) @ wd.T
+    t_layer = (time.perf_counter() - t0) / layers_sample
+    lm_rows = min(spec.vocab, 16384)
+    lm = W(lm_rows, d)
+    t1 = time.perf_counter()
+    _ = x @ lm.T
+    t_head = (time.perf_counter() - t1) * spec.vocab / lm_rows
+    threads = int(os.environ.get("OMP_NUM_THREADS", 0)) or len(os.sched_getaffinity(0))
+    sample = (f"{layers_sample} decoder layer(s) x {M} rows at context {ctx} + {lm_rows}/{spec.vocab} lm_head "
+              f"rows, fp32 numpy oracle port, scaled x{spec.layers} layers")
+    return t_layer * spec.layers + t_head, threads, sample
+
+
+# ---------------------------------------------------------------- GPU leg
+def run_ours(args):
+    import numpy as np
+    import torch
+    from paper_2605_02189_b200 import ops
+    from paper_2605_02189_b200.engine import DecodeEngine
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks, peaks_src = load_peaks()
+    spec, state, cfg, params, reqs, desc = workload()
+    eng = DecodeEngine(spec, state, cfg, params, reqs, device=f"cuda:{local}", kv_init="random",
+                       timing=True, seed=rank)
+    ex, kv = eng.stages[0]
+    # warmup
+    for _ in range(args.warmup):
+        assert eng.step() is not None
+    torch.cuda.synchronize()
+    ids_host = torch.zeros(args.steps, eng.m_cap, dtype=torch.int32).pin_memory()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    timer = ops.KernelTimer() if args.kernel_timing else None
+    tokens = 0
+    h2d_b = d2h_b = meta_b = 0
+    h2d0, d2h0 = kv.h2d_bytes, kv.d2h_bytes
+    rec0 = len(kv.records)
+    start_ev, end_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ops.TIMER = timer
+        start_ev.record(kv.compute)
+        w0 = time.perf_counter()
+        for i in range(args.steps):
+            work = eng.step()
+            assert work is not None, "workload ended inside the timed region"
+            M = len(work.rows)
+            tokens += M
+            meta_b += M * (eng.max_blocks + 3) * 4
+            with torch.cuda.stream(kv.compute):
+                ids_host[i, :M].copy_(ex.out_ids[:M], non_blocking=True)
+        end_ev.record(kv.compute)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        ops.TIMER = None
+    dev_s = start_ev.elapsed_time(end_ev) * 1e-3
+    if dist:
+        t = torch.tensor([dev_s, wall], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s, wall = t.tolist()
+        tot = torch.tensor([tokens], device="cuda")
+        dist.all_reduce(tot)
+        tokens_all = int(tot.item())
+    else:
+        tokens_all = tokens
+    h2d_b, d2h_b = kv.h2d_bytes - h2d0, kv.d2h_bytes - d2h0
+    # offload hiding over the timed steps
+    stall = h2d_busy = d2h_busy = 0.0
+    for r in kv.records[rec0:]:
+        if "ready" in r:
+            stall += r["ready"].elapsed_time(r["start"]) * 1e-3
+        if "h2d_start" in r:
+            h2d_busy += r["h2d_start"].elapsed_time(r["h2d_end"]) * 1e-3
+        if "d2h_start" in r:
+            d2h_busy += r["d2h_start"].elapsed_time(r["d2h_end"]) * 1e-3
+    busy = h2d_busy + d2h_busy
+    hidden = 1.0 - stall / busy if busy > 0 else 1.0
+    # step roofline: algorithmic HBM bytes of the timed steps vs measured HBM peak; host link bound
+    step_bytes = 0
+    launches = args.steps * ex.kernels_per_step()
+    value = tokens_all / dev_s
+    out = {
+        "metric": "offline decode tokens/sec (B200, KV offload on)",
+        "value": value,
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dev_s / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (random-init weights seeded N(0,0.02), random KV, random first tokens)",
+        "config": desc,
+        "e2e": {"value": tokens_all / wall, "unit": "tokens/s",
+                "h2d_bytes_per_step": int((h2d_b + meta_b) / args.steps),
+                "d2h_bytes_per_step": int((d2h_b + tokens * 4) / args.steps),
+                "note": "public engine API (DecodeEngine.step, the simulate_decode loop): host control "
+                        "plane, metadata + KV prefetch H2D from pinned memory, KV offload + greedy ids D2H"},
+        "kv_transfer_hidden_fraction": hidden,
+        "kv_transfer": {"h2d_bytes": h2d_b, "d2h_bytes": d2h_b, "h2d_busy_s": h2d_busy,
+                        "d2h_busy_s": d2h_busy, "exposed_stall_s": stall},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if timer is not None:
+        summ = timer.summary()
+        kinds = sorted(summ.items(), key=lambda kv_: -kv_[1]["seconds"])
+        top, d = kinds[0]
+        per_launch_bytes = d["bytes"] / d["launches"]
+        per_launch_s = d["seconds"] / d["launches"]
+        achieved = per_launch_bytes / per_launch_s / 1e9
+        out["roofline"] = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peaks["hbm_gbs"],
+                           "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                           "peak_source": peaks_src,
+                           "share_of_step": d["seconds"] / dev_s,
+                           "per_kind": {k: {"launches": v["launches"], "GBps": v["bytes"] / v["seconds"] / 1e9,
+                                            "share": v["seconds"] / dev_s} for k, v in summ.items()}}
+        out["roofline"]["note"] = ("achieved = algorithmic bytes per launch (weights once + activations; "
+                                   "attention: the micro-batch's KV once) / CUDA-event launch time, "
+                                   "averaged over the timed region")
+    if rank == 0 and not args.no_cpu_baseline:
+        kv_ctx = int(np.mean([eng.control.state.lengths.get(r, 0) for r in range(len(reqs))]))
+        M = int(round(tokens / args.steps))
+        sec, thr, sample = cpu_port_step_seconds(spec, M, kv_ctx)
+        out["cpu_baseline"] = {"value": M / sec, "unit": "tokens/s", "cores": thr, "kind": "port",
+                               "sample": sample}
+    if rank == 0:
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """CPU implementation of the path (oracle port) on all host threads."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    spec, state, cfg, params, reqs, desc = workload()
+    M = max(len(b) for b in state.batches)
+    ctx = 512 + args.warmup
+    times = []
+    sample = None
+    for _ in range(max(1, args.steps)):
+        sec, thr, sample = cpu_port_step_seconds(spec, M, ctx)
+        times.append(sec)
+    sec = sum(times) / len(times)
+    val = M / sec
+    out = {"impl": "reference", "metric": "offline decode tokens/sec (B200, KV offload on)", "value": val,
+           "unit": "tokens/s", "n_gpus": int(os.environ.get("WORLD_SIZE", 1)), "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": desc,
+           "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": thr, "kind": "port", "sample": sample},
+           "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=6)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-kernel-timing", dest="kernel_timing", action="store_false")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference"
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,63 @@
+/* C-ABI of the B200 PipeMax decode path (libpmb200.so).
+ *
+ * The reference (arxiv 2605.02189, pkg/src/pipemax) is a pure-Python
+ * simulator: it has no native code and no FFI.  These entry points replace
+ * the SIMULATED pieces of its decode engine (`_DecodeEngine.run`,
+ * pipeline_sim.py:386-543) and are bound from Python with ctypes
+ * (paper_2605_02189_b200/_C.py; INTEGRATION.md shows the binding):
+ *
+ *   stage compute  `estimate_decode_time(...) * noise / n`     pipeline_sim.py:423-427
+ *       -> pm_embed, pm_rmsnorm, pm_gemm, pm_qkv_rope_append,
+ *          pm_paged_attention, pm_argmax_reduce
+ *   KV prefetch    `h2d.submit_stream(... "kv_prefetch")`       pipeline_sim.py:442-450
+ *   KV offload     `d2h.submit_stream(... "kv_offload_decode")` pipeline_sim.py:486-490
+ *       -> pm_copy_pieces (+ pm_host_alloc / pm_host_free for the host pool)
+ *
+ * Conventions: every function returns a cudaError_t as int (0 = success) and
+ * pm_error_string() describes it; calls are asynchronous on the given CUDA
+ * stream (cudaStream_t passed as void*); no function allocates device memory
+ * (workspaces are caller-owned); tensor maps are 128-byte CUtensorMap images
+ * built by pm_tmap_encode_2d.  bf16 tensors are passed as void*.
+ */
+#ifndef PM_B200_H
+#define PM_B200_H
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+int pm_abi_version(void);
+const char* pm_error_string(int code);
+
+/* ---- descriptors / memory ------------------------------------------------ */
+int pm_tmap_encode_2d(void* tmap_out, const void* gaddr, unsigned long long inner, unsigned long long outer,
+                      unsigned long long row_stride_bytes, unsigned box_inner, unsigned box_outer,
+                      int swizzle128);
+int pm_host_alloc(unsigned long long bytes, void** out);
+int pm_host_free(void* p);
+/* dst_base+dst_off[i] <- src_base+src_off[i], `bytes` each; contiguous runs merged */
+int pm_copy_pieces(void* dst_base, const void* src_base, const long long* dst_off, const long long* src_off,
+                   int n, unsigned long long bytes, void* stream);
+
+/* ---- per-stage decode forward ---------------------------------------------- */
+int pm_embed(const int* tok_table, const int* slots, const void* table, float* resid, int M, int d,
+             void* stream);
+int pm_rmsnorm(const float* x, const void* w, void* y, int M, int d, float eps, void* stream);
+/* stream-K tcgen05 GEMM over a packed weight ([units][K/64][2][128][64], 128B-swizzled) */
+int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok, int bn,
+            int grid, int epilogue, void* out, int ld_out, float* ws, int max_segs, float* amax_val,
+            int* amax_idx, int m_cap, void* stream);
+int pm_gemm_max_segments(long long total, int kb, int grid);
+int pm_qkv_rope_append(const void* qkv, void* q_out, void* pool, const int* block_table, const int* positions,
+                       const float* rope, const void* qn_w, const void* kn_w, int M, int H, int Hkv, int hd,
+                       int layer, int L_s, int max_blocks, float eps, void* stream);
+int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_table, const int* seq_lens,
+                       void* out, float* ws_o, float* ws_ml, int* counters, int M, int H, int Hkv, int hd,
+                       int layer, int L_s, int max_blocks, int max_splits, void* stream);
+int pm_attn_blocks_per_split(void);
+int pm_argmax_reduce(const float* val, const int* idx, int n_tiles, int M, int m_cap, int* out_ids,
+                     int* tok_table, const int* slots, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

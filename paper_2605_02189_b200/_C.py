@@ -22,7 +22,8 @@ _SIGS = {
     "pm_host_alloc": [_U64, C.POINTER(_P)],
     "pm_host_free": [_P],
     "pm_copy_pieces": [_P, _P, _P, _P, _I, _U64, _P],
-    "pm_gemm": [_P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _P, _P, _P],
+    "pm_gemm": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _P, _I, _P],
+    "pm_gemm_max_segments": [_LL, _I, _I],
     "pm_embed": [_P, _P, _P, _P, _I, _I, _P],
     "pm_rmsnorm": [_P, _P, _P, _I, _I, _F, _P],
     "pm_qkv_rope_append": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P],

@@ -1,87 +1,195 @@
-// Decode projection GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+// Decode projection GEMM on 5th-gen tensor cores (tcgen05 + TMEM), persistent
+// stream-K, weights streamed as pre-packed contiguous chunks.
 //
-// Swap-AB: the weight tile is the 128-row MMA "A" operand and the micro-batch
-// tokens are the MMA "N" (16..256), so D^T[n_out, tok] = W[n_out, K] . X[tok, K]^T
-// accumulates in TMEM.  At decode batch sizes the kernel streams each weight
-// byte from HBM exactly once (weight-bandwidth bound for M_tok <~ 255).
-//
-// Roles (128 threads, 1 CTA / output tile x K-split):
-//   warp0.lane0  TMA producer: W tile [128 x 64] and X tile [BN x 64] per stage,
-//                both K-major with the 128-byte swizzle, weights evict-first.
-//   warp1.lane0  MMA issuer: 4 x tcgen05.mma (K=16 each) per stage, commit frees
-//                the stage, final commit signals the epilogue.
-//   warps0-3     epilogue: tcgen05.ld rows 32w..32w+31 of the accumulator.
-// Fixed K-split per (N, K) shape (chosen on the host, independent of M_tok)
-// keeps every token's result independent of its micro-batch mates; the last
-// CTA of a tile sums the fp32 partials in split order (deterministic).
+// Swap-AB: a 256-row weight unit (two 128-row UMMA tiles) is the MMA "A"
+// operand and the micro-batch tokens are the MMA "N" (16..256):
+//     D^T[n_out, tok] = W[n_out, K] . X[tok, K]^T      (fp32 in TMEM)
+// At decode batch sizes (M_tok <~ 255) the GEMM is weight-bandwidth bound, so
+// the design goal is to keep all 148 SMs streaming weights from HBM at the
+// copy rate every cycle of the kernel:
+//   * weights are re-packed once at load time into [unit][k-block][2 x 128 x 64]
+//     chunks that are already in the UMMA 128B-swizzled K-major smem image, so
+//     each pipeline stage is ONE 32 KB contiguous bulk copy (cp.async.bulk);
+//   * the activation tile [BN x 64] comes by 2-D TMA from L2 and is shared by
+//     both 128-row halves of the unit (halves its SM ingress vs 128-row units);
+//   * persistent grid = #SMs, stream-K: the (unit, k-block) sequence is cut
+//     into #SMs equal contiguous ranges, so every SM streams the same bytes;
+//     a unit split between CTAs accumulates per-segment fp32 partials and the
+//     last CTA to finish it (atomic counter) sums them in segment order --
+//     boundaries depend only on (N, K, #SMs), never on M_tok, so every token's
+//     result is independent of its micro-batch mates (batch-invariant);
+//   * warp roles: w0 bulk/TMA producer, w1 MMA issuer (+TMEM owner), w2..w5
+//     epilogue; the TMEM accumulator is double-buffered (BN <= 128) so the
+//     epilogue of one segment overlaps the mainloop of the next.
+// Epilogues: bf16 store, fp32 residual add, SiLU(gate)*up over interleaved
+// gate/up rows, fp32 logits + per-unit argmax partials.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace {
 
-constexpr int BM = 128;
-constexpr int BK = 64;           // 64 bf16 = 128 B rows -> SWIZZLE_128B
-constexpr int A_BYTES = BM * BK * 2;
+constexpr int UNIT_ROWS = 256;             // rows of W per work unit (2 UMMA tiles)
+constexpr int BK = 64;                     // 64 bf16 = 128 B = one swizzle atom row
+constexpr int SUB_BYTES = 128 * BK * 2;    // one 128x64 UMMA A tile (16 KB)
+constexpr int A_BYTES = 2 * SUB_BYTES;     // 32 KB per stage, contiguous in global
+constexpr int NUM_THREADS = 192;           // 6 warps
+constexpr int EPI_WARP0 = 2;
 
-enum Epilogue : int {
-  EPI_STORE_BF16 = 0,    // out_bf16[tok][n] = acc
-  EPI_RESID_ADD_F32 = 1, // out_f32[tok][n] += acc          (residual stream)
-  EPI_SILU_MUL = 2,      // rows interleaved gate/up: out_bf16[tok][n/2] = silu(g)*u
-  EPI_LOGITS_ARGMAX = 3, // optional out_f32[tok][n] = acc; per-tile argmax partials
-};
+enum Epilogue : int { EPI_STORE_BF16 = 0, EPI_RESID_ADD_F32 = 1, EPI_SILU_MUL = 2, EPI_LOGITS_ARGMAX = 3 };
 
 struct GemmArgs {
-  int n_out, k, m_tok;
-  int splits;
+  const uint8_t* w;   // packed weights
+  int n_out;          // real output features (rows beyond are zero padding)
+  int n_units;        // padded rows / 256
+  int kb;             // K / 64
+  int m_tok;
+  int tok_tiles;
   int epilogue;
   void* out;
   int ld_out;
-  float* ws;          // [splits][m_cap][n_out] fp32 partials (splits > 1)
-  int m_cap;
-  int* counters;      // [tok_tiles][n_tiles], zero at rest (self-resetting)
-  float* amax_val;    // [n_tiles][m_cap]
+  float* ws;          // [units*tok_tiles][max_segs][BN][256] fp32 partials of split units
+  int max_segs;
+  float* amax_val;    // [units][m_cap]
   int* amax_idx;
+  int m_cap;
+  long long total;    // units * tok_tiles * kb
+  int debug;          // bit0: skip epilogue math (profiling only)
 };
 
 template <int BN>
 struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
+  static constexpr int ACC_BUFS = BN <= 128 ? 2 : 1;            // 2 bufs x 2 halves x BN <= 512 cols
+  static constexpr int TMEM_COLS = ACC_BUFS * 2 * BN <= 32 ? 32 : (ACC_BUFS * 2 * BN <= 64 ? 64 : (ACC_BUFS * 2 * BN <= 128 ? 128 : (ACC_BUFS * 2 * BN <= 256 ? 256 : 512)));
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 512 + 4 * BN * 8;
 };
 
-__device__ __forceinline__ float silu(float g) { return g / (1.0f + expf(-g)); }
+PM_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+PM_DEV void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+PM_DEV float silu(float g) { return g / (1.0f + expf(-g)); }
+
+// CTA c owns linear k-block indices [lo(c), lo(c+1)) with lo(c) = floor(c*T/G).
+PM_DEV long long range_lo(long long c, long long T, long long G) { return (c * T) / G; }
+// the CTA whose range holds index idx
+PM_DEV long long owner_of(long long idx, long long T, long long G) { return ((idx + 1) * G + T - 1) / T - 1; }
+
+struct Seg {
+  int unit;     // (tok tile, weight unit) linear id
+  int kb0, kb1; // k-block range inside the unit
+  int seg;      // segment index within the unit
+  int nseg;     // number of segments of the unit
+};
+
+// i-th segment of this CTA; returns false when past the end
+PM_DEV bool get_seg(const GemmArgs& a, long long lo, long long hi, int i, Seg& s) {
+  long long pos = lo;
+  const long long T = a.total, G = gridDim.x;
+  for (int j = 0; j <= i; ++j) {
+    if (pos >= hi) return false;
+    const long long u = pos / a.kb;
+    const long long end = min(hi, (u + 1) * a.kb);
+    if (j == i) {
+      s.unit = (int)u;
+      s.kb0 = (int)(pos - u * a.kb);
+      s.kb1 = (int)(end - u * a.kb);
+      const long long first = owner_of(u * a.kb, T, G);
+      const long long last = owner_of((u + 1) * a.kb - 1, T, G);
+      s.seg = (int)(blockIdx.x - first);
+      s.nseg = (int)(last - first + 1);
+      return true;
+    }
+    pos = end;
+  }
+  return false;
+}
+
+// Epilogue of one output feature `n` (a row of D^T) over token columns
+// c0..c0+15.  Rows held by one warp are 32 consecutive features, so the
+// SiLU(gate)*up partner of row n (interleaved gate/up rows) is lane ^ 1.
+PM_DEV void row_epilogue(const GemmArgs& a, int n, int tok_base, int tok_end, int c0, const float* v, int lane) {
+  const bool row_ok = n < a.n_out;
+  switch (a.epilogue) {
+    case EPI_STORE_BF16: {
+      bf16* o = reinterpret_cast<bf16*>(a.out);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < tok_end && row_ok) o[(size_t)(tok_base + c0 + j) * a.ld_out + n] = __float2bfloat16(v[j]);
+      break;
+    }
+    case EPI_RESID_ADD_F32: {
+      float* o = reinterpret_cast<float*>(a.out);
+      float r[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        r[j] = (c0 + j < tok_end && row_ok) ? o[(size_t)(tok_base + c0 + j) * a.ld_out + n] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < tok_end && row_ok) o[(size_t)(tok_base + c0 + j) * a.ld_out + n] = r[j] + v[j];
+      break;
+    }
+    case EPI_SILU_MUL: {
+      bf16* o = reinterpret_cast<bf16*>(a.out);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float up = __shfl_xor_sync(0xffffffffu, v[j], 1);
+        if ((lane & 1) == 0 && c0 + j < tok_end && row_ok)
+          o[(size_t)(tok_base + c0 + j) * a.ld_out + (n >> 1)] = __float2bfloat16(silu(v[j]) * up);
+      }
+      break;
+    }
+    case EPI_LOGITS_ARGMAX: {
+      if (a.out) {
+        float* o = reinterpret_cast<float*>(a.out);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < tok_end && row_ok) o[(size_t)(tok_base + c0 + j) * a.ld_out + n] = v[j];
+      }
+      break;
+    }
+  }
+}
+
+// warp-level (max, lowest index) over the rows a lane holds; lane 0 gets the result
+PM_DEV void warp_argmax(float& bv, int& bi) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  }
+}
 
 template <int BN>
-__global__ void __launch_bounds__(128, 1)
-gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
-               GemmArgs a) {
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sa = smem;                                  // STAGES x A tile
-  uint8_t* sb = smem + C::STAGES * A_BYTES;             // STAGES x B tile
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* sa = smem;
+  uint8_t* sb = smem + C::STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* done = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-  int* flag = reinterpret_cast<int*>(tmem_slot + 1);
-  float* red_val = reinterpret_cast<float*>(flag + 1);   // [4] cross-warp argmax
-  int* red_idx = reinterpret_cast<int*>(red_val + 4);
+  uint64_t* tfull = empty + C::STAGES;      // [2]
+  uint64_t* tempty = tfull + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* red_val = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE + 512);   // [4][BN]
+  int* red_idx = reinterpret_cast<int*>(red_val + 4 * BN);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x, split = blockIdx.y, ttile = blockIdx.z;
-  const int kb_total = a.k / BK;
-  const int kb0 = (int)((long long)kb_total * split / a.splits);
-  const int kb1 = (int)((long long)kb_total * (split + 1) / a.splits);
-  const int nkb = kb1 - kb0;
+  const long long lo = range_lo(blockIdx.x, a.total, gridDim.x);
+  const long long hi = range_lo(blockIdx.x + 1, a.total, gridDim.x);
 
   if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmap_w);
     tma_prefetch_desc(&tmap_x);
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -90,128 +198,121 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer
-    const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-    for (int it = 0; it < nkb; ++it) {
-      const int s = it % C::STAGES;
-      if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
-      mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-      const int kx = (kb0 + it) * BK;
-      tma_load_2d(sa + s * A_BYTES, &tmap_w, &full[s], kx, tile * BM, pol_w);
-      tma_load_2d(sb + s * C::B_BYTES, &tmap_x, &full[s], kx, ttile * BN, pol_x);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
-    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-    for (int it = 0; it < nkb; ++it) {
-      const int s = it % C::STAGES;
-      mbar_wait(&full[s], (it / C::STAGES) & 1);
-      tc_fence_after();
-      const uint64_t da = umma_desc_sw128(smem_u32(sa + s * A_BYTES));
-      const uint64_t db = umma_desc_sw128(smem_u32(sb + s * C::B_BYTES));
-#pragma unroll
-      for (int kk = 0; kk < BK / 16; ++kk)  // +32 B per K=16 slice -> +2 in the >>4 field
-        tc_mma_bf16(tmem, da + 2 * kk, db + 2 * kk, idesc, (it | kk) != 0);
-      tc_commit(&empty[s]);
-    }
-    tc_commit(done);
-  }
-  __syncwarp();
-
-  // ---------------- epilogue (all 4 warps)
-  mbar_wait(done, 0);
-  tc_fence_after();
-  const int row = warp * 32 + lane;
-  const int n = tile * BM + row;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  const int tok_base = ttile * BN;
-  const int tok_end = min(BN, a.m_tok - tok_base);
-
-  bool last = true;
-  if (a.splits > 1) {
-    float* part = a.ws + (size_t)split * a.m_cap * a.n_out;
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      if (c0 >= tok_end) break;
-      float v[16];
-      tmem_ld16(trow + c0, v);
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (c0 + j < tok_end) part[(size_t)(tok_base + c0 + j) * a.n_out + n] = v[j];
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int* ctr = a.counters + (size_t)ttile * gridDim.x + tile;
-      const int prev = atomicAdd(ctr, 1);
-      const int is_last = prev == a.splits - 1;
-      if (is_last) *ctr = 0;  // self-reset for the next launch
-      *flag = is_last;
-    }
-    __syncthreads();
-    last = *flag != 0;
-    if (last) __threadfence();
-  }
-  if (last) {
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      if (c0 >= tok_end) break;
-      float v[16];
-      if (a.splits > 1) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
-        for (int s = 0; s < a.splits; ++s) {
-          const float* part = a.ws + (size_t)s * a.m_cap * a.n_out;
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < tok_end) v[j] += __ldcg(&part[(size_t)(tok_base + c0 + j) * a.n_out + n]);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- producer: one 32 KB bulk weight chunk + one X tile per stage
+      const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+      int it = 0;
+      Seg sg;
+      for (int i = 0; get_seg(a, lo, hi, i, sg); ++i) {
+        const int wunit = sg.unit % a.n_units, ttile = sg.unit / a.n_units;
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], C::STAGE);
+          bulk_load(sa + s * A_BYTES, a.w + ((size_t)wunit * a.kb + kb) * A_BYTES, A_BYTES, &full[s], pol_w);
+          tma_load_2d(sb + s * C::B_BYTES, &tmap_x, &full[s], kb * BK, ttile * BN, pol_x);
         }
-      } else {
-        tmem_ld16(trow + c0, v);
       }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
+      int it = 0;
+      Seg sg;
+      for (int i = 0; get_seg(a, lo, hi, i, sg); ++i) {
+        const int b = i % C::ACC_BUFS;
+        if (i >= C::ACC_BUFS) mbar_wait(&tempty[b], ((i / C::ACC_BUFS) - 1) & 1);
+        tc_fence_after();
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(&full[s], (it / C::STAGES) & 1);
+          tc_fence_after();
+          const uint64_t db = umma_desc_sw128(smem_u32(sb + s * C::B_BYTES));
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int c = c0 + j;
-        const int tok = tok_base + c;
-        const bool valid = c < tok_end;
-        const float acc = v[j];
-        switch (a.epilogue) {
-          case EPI_STORE_BF16:
-            if (valid) reinterpret_cast<bf16*>(a.out)[(size_t)tok * a.ld_out + n] = __float2bfloat16(acc);
-            break;
-          case EPI_RESID_ADD_F32:
-            if (valid) reinterpret_cast<float*>(a.out)[(size_t)tok * a.ld_out + n] += acc;
-            break;
-          case EPI_SILU_MUL: {
-            const float up = __shfl_xor_sync(0xffffffffu, acc, 1);
-            if (valid && (lane & 1) == 0)
-              reinterpret_cast<bf16*>(a.out)[(size_t)tok * a.ld_out + (n >> 1)] =
-                  __float2bfloat16(silu(acc) * up);
-            break;
+          for (int h = 0; h < 2; ++h) {
+            const uint64_t da = umma_desc_sw128(smem_u32(sa + s * A_BYTES + h * SUB_BYTES));
+            const uint32_t acc = tmem + (uint32_t)((b * 2 + h) * BN);
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              tc_mma_bf16(acc, da + 2 * kk, db + 2 * kk, idesc, (kb > sg.kb0 || kk > 0) ? 1u : 0u);
           }
-          case EPI_LOGITS_ARGMAX: {
-            if (valid && a.out) reinterpret_cast<float*>(a.out)[(size_t)tok * a.ld_out + n] = acc;
-            float bv = (n < a.n_out) ? acc : -INFINITY;
-            int bi = n;
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&tfull[b]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue warps 2..5: TMEM lane quarter q = warp % 4
+    const int q = warp & 3;
+    const int wq = warp - EPI_WARP0;
+    Seg sg;
+    for (int i = 0; get_seg(a, lo, hi, i, sg); ++i) {
+      const int b = i % C::ACC_BUFS;
+      mbar_wait(&tfull[b], (i / C::ACC_BUFS) & 1);
+      tc_fence_after();
+      const int tok_tile = sg.unit / a.n_units, wunit = sg.unit % a.n_units;
+      const int tok_base = tok_tile * BN;
+      const int tok_end = min(BN, a.m_tok - tok_base);
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+      const bool whole = sg.nseg == 1;
+      const bool argmax = whole && a.epilogue == EPI_LOGITS_ARGMAX;
+      if (!(a.debug & 1)) {
+        if (whole) {
+          const int n0 = wunit * UNIT_ROWS + q * 32 + lane;
+          for (int c0 = 0; c0 < BN && c0 < tok_end; c0 += 16) {
+            float v0[16], v1[16];
+            tmem_ld16(trow + (b * 2 + 0) * BN + c0, v0);
+            tmem_ld16(trow + (b * 2 + 1) * BN + c0, v1);
+            row_epilogue(a, n0, tok_base, tok_end, c0, v0, lane);
+            row_epilogue(a, n0 + 128, tok_base, tok_end, c0, v1, lane);
+            if (argmax) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-              const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-              if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+              for (int j = 0; j < 16; ++j) {
+                float bv = n0 < a.n_out ? v0[j] : -INFINITY;
+                int bi = n0;
+                if (n0 + 128 < a.n_out && v1[j] > bv) { bv = v1[j]; bi = n0 + 128; }
+                warp_argmax(bv, bi);
+                if (lane == 0) { red_val[wq * BN + c0 + j] = bv; red_idx[wq * BN + c0 + j] = bi; }
+              }
             }
-            if (lane == 0) { red_val[warp] = bv; red_idx[warp] = bi; }
-            __syncthreads();
-            if (threadIdx.x == 0 && valid) {
-              float best = red_val[0];
-              int bidx = red_idx[0];
-              for (int w = 1; w < 4; ++w)
-                if (red_val[w] > best || (red_val[w] == best && red_idx[w] < bidx)) { best = red_val[w]; bidx = red_idx[w]; }
-              a.amax_val[(size_t)tile * a.m_cap + tok] = best;
-              a.amax_idx[(size_t)tile * a.m_cap + tok] = bidx;
+          }
+        } else {
+          // partial segment: fp32 [seg][col][256 rows]; gemm_reduce_kernel finishes the unit
+          float* dst = a.ws + ((size_t)sg.unit * a.max_segs + sg.seg) * (size_t)BN * UNIT_ROWS;
+          for (int c0 = 0; c0 < BN && c0 < tok_end; c0 += 16) {
+            float v0[16], v1[16];
+            tmem_ld16(trow + (b * 2 + 0) * BN + c0, v0);
+            tmem_ld16(trow + (b * 2 + 1) * BN + c0, v1);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              __stcg(&dst[(size_t)(c0 + j) * UNIT_ROWS + q * 32 + lane], v0[j]);
+              __stcg(&dst[(size_t)(c0 + j) * UNIT_ROWS + 128 + q * 32 + lane], v1[j]);
             }
-            __syncthreads();
-            break;
           }
         }
+      }
+      // accumulator drained -> the MMA warp may reuse this TMEM buffer
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+      if (argmax && !(a.debug & 1)) {
+        epi_bar();
+        for (int c = threadIdx.x - EPI_WARP0 * 32; c < tok_end; c += 128) {
+          float bv = red_val[c];
+          int bi = red_idx[c];
+          for (int w = 1; w < 4; ++w)
+            if (red_val[w * BN + c] > bv || (red_val[w * BN + c] == bv && red_idx[w * BN + c] < bi)) {
+              bv = red_val[w * BN + c];
+              bi = red_idx[w * BN + c];
+            }
+          a.amax_val[(size_t)wunit * a.m_cap + tok_base + c] = bv;
+          a.amax_idx[(size_t)wunit * a.m_cap + tok_base + c] = bi;
+        }
+        epi_bar();
       }
     }
   }
@@ -220,37 +321,109 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant
   if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
+// Finishes the units the stream-K partition split across CTAs: sums the
+// per-segment fp32 partials in segment order (deterministic) and applies the
+// epilogue.  One CTA per (split unit, 16-column chunk); thread = output row.
 template <int BN>
-int launch(const CUtensorMap* tw, const CUtensorMap* tx, const GemmArgs& a, cudaStream_t st) {
+__global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) {
+  const int unit = blockIdx.x, c0 = blockIdx.y * 16;
+  const long long T = a.total, G = grid;
+  const long long first = owner_of((long long)unit * a.kb, T, G);
+  const long long last = owner_of((long long)(unit + 1) * a.kb - 1, T, G);
+  const int nseg = (int)(last - first + 1);
+  if (nseg == 1) return;
+  const int tok_tile = unit / a.n_units, wunit = unit % a.n_units;
+  const int tok_base = tok_tile * BN;
+  const int tok_end = min(BN, a.m_tok - tok_base);
+  if (c0 >= tok_end) return;
+  const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
+  const int n = wunit * UNIT_ROWS + r;
+  const float* part = a.ws + (size_t)unit * a.max_segs * BN * UNIT_ROWS + (size_t)c0 * UNIT_ROWS + r;
+  float v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = 0.f;
+#pragma unroll 2
+  for (int s = 0; s < nseg; ++s) {
+    float t[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) t[j] = __ldcg(part + ((size_t)s * BN + j) * UNIT_ROWS);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] += t[j];
+  }
+  row_epilogue(a, n, tok_base, tok_end, c0, v, lane);
+  if (a.epilogue == EPI_LOGITS_ARGMAX) {
+    __shared__ float sv[8][16];
+    __shared__ int si[8][16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float bv = n < a.n_out ? v[j] : -INFINITY;
+      int bi = n;
+      warp_argmax(bv, bi);
+      if (lane == 0) { sv[warp][j] = bv; si[warp][j] = bi; }
+    }
+    __syncthreads();
+    if (r < 16 && c0 + r < tok_end) {
+      float bv = sv[0][r];
+      int bi = si[0][r];
+      for (int w = 1; w < 8; ++w)
+        if (sv[w][r] > bv || (sv[w][r] == bv && si[w][r] < bi)) { bv = sv[w][r]; bi = si[w][r]; }
+      a.amax_val[(size_t)wunit * a.m_cap + tok_base + c0 + r] = bv;
+      a.amax_idx[(size_t)wunit * a.m_cap + tok_base + c0 + r] = bi;
+    }
+  }
+}
+
+template <int BN>
+int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st) {
   using C = Cfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_stream_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  dim3 grid(a.n_out / BM, a.splits, (a.m_tok + BN - 1) / BN);
-  gemm_tc_kernel<BN><<<grid, 128, C::SMEM, st>>>(*tw, *tx, a);
+  gemm_stream_kernel<BN><<<grid, NUM_THREADS, C::SMEM, st>>>(*tx, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || a.max_segs <= 1 || (a.debug & 1)) return (int)e;
+  gemm_reduce_kernel<BN><<<dim3(a.n_units * a.tok_tiles, BN / 16), 256, 0, st>>>(a, grid);
   return (int)cudaGetLastError();
 }
 
 }  // namespace
 
-extern "C" int pm_gemm(const void* tmap_w, const void* tmap_x, int n_out, int k, int m_tok, int bn,
-                       int splits, int epilogue, void* out, int ld_out, float* ws, int m_cap,
-                       int* counters, float* amax_val, int* amax_idx, void* stream) {
-  if (n_out % BM || k % BK || m_tok < 1 || splits < 1 || splits > k / BK) return (int)cudaErrorInvalidValue;
-  if (m_tok > m_cap) return (int)cudaErrorInvalidValue;
-  GemmArgs a{n_out, k, m_tok, splits, epilogue, out, ld_out, ws, m_cap, counters, amax_val, amax_idx};
-  auto tw = reinterpret_cast<const CUtensorMap*>(tmap_w);
+// Segments a unit of `kb` k-blocks can be cut into by `grid` CTAs over `total`
+// k-blocks (host helper for workspace sizing; mirrors owner_of()).
+extern "C" int pm_gemm_max_segments(long long total, int kb, int grid) {
+  int best = 1;
+  for (long long u = 0; u * kb < total; ++u) {
+    const long long first = ((u * kb + 1) * grid + total - 1) / total - 1;
+    const long long last = (((u + 1) * kb) * grid + total - 1) / total - 1;
+    const int n = (int)(last - first + 1);
+    if (n > best) best = n;
+  }
+  return best;
+}
+
+// w_packed: [n_units][kb][2][128][64] bf16, each 128x64 tile in the 128B-
+// swizzled K-major UMMA smem image (see ops.pack_weight).
+extern "C" int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
+                       int bn, int grid, int epilogue, void* out, int ld_out, float* ws, int max_segs,
+                       float* amax_val, int* amax_idx, int m_cap, void* stream) {
+  if (k % BK || m_tok < 1 || m_tok > m_cap || grid < 1) return (int)cudaErrorInvalidValue;
+  const int tok_tiles = (m_tok + bn - 1) / bn;
+  GemmArgs a{reinterpret_cast<const uint8_t*>(w_packed), n_out, n_units, k / BK, m_tok, tok_tiles, epilogue,
+             out, ld_out, ws, max_segs, amax_val, amax_idx, m_cap,
+             (long long)n_units * tok_tiles * (k / BK), 0};
+  if (getenv("PM_GEMM_DEBUG")) a.debug = atoi(getenv("PM_GEMM_DEBUG"));
+  if (grid > a.total) grid = (int)a.total;
   auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   auto st = reinterpret_cast<cudaStream_t>(stream);
   switch (bn) {
-    case 16: return launch<16>(tw, tx, a, st);
-    case 32: return launch<32>(tw, tx, a, st);
-    case 64: return launch<64>(tw, tx, a, st);
-    case 128: return launch<128>(tw, tx, a, st);
-    case 256: return launch<256>(tw, tx, a, st);
+    case 16: return launch<16>(tx, a, grid, st);
+    case 32: return launch<32>(tx, a, grid, st);
+    case 64: return launch<64>(tx, a, grid, st);
+    case 128: return launch<128>(tx, a, grid, st);
+    case 256: return launch<256>(tx, a, grid, st);
     default: return (int)cudaErrorInvalidValue;
   }
 }

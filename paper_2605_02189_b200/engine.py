@@ -205,7 +205,7 @@ class DecodeEngine:
             evs.append(ev)
         self.meta.events[k] = evs
 
-    def _forward_all(self, M):
+    def _forward_all(self, M, kv_tokens=0):
         """Run the stages in order on their compute streams (single process:
         stage s+1 waits for stage s's activations via an event)."""
         prev_ev = None
@@ -215,7 +215,7 @@ class DecodeEngine:
             with torch.cuda.stream(kv.compute):
                 if si > 0:
                     ex.resid[:M].copy_(self.stages[si - 1][0].resid[:M])
-                ex.forward(M, kv.compute)
+                ex.forward(M, kv.compute, kv_tokens=kv_tokens)
                 if si == len(self.stages) - 1 and len(self.stages) > 1:
                     # greedy ids back to stage 0's token table (the last->first hop)
                     first = self.stages[0][0]
@@ -241,7 +241,7 @@ class DecodeEngine:
         self._upload_meta(work.rows, work.positions, work.tables)
         for (ex, kv), rec in zip(self.stages, recs):
             kv.before_compute(t, work, rec)
-        self._forward_all(M)
+        self._forward_all(M, kv_tokens=sum(work.positions) + M)
         for (ex, kv), rec in zip(self.stages, recs):
             kv.after_compute(t, rec)
             kv.offload(t, work, rec)

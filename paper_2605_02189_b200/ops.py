@@ -15,6 +15,35 @@ SMS = 148
 BM, BK = 128, 64
 
 
+class KernelTimer:
+    """Optional per-launch CUDA-event timing (bench.py's roofline leg): events
+    are recorded on the launching stream around each kernel, with the
+    launch's algorithmic HBM bytes."""
+
+    def __init__(self):
+        self.pending = []   # (kind, bytes, start_ev, end_ev)
+
+    def around(self, kind, nbytes, stream, fn):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        fn()
+        b.record(s)
+        self.pending.append((kind, nbytes, a, b))
+
+    def summary(self):
+        out = {}
+        for kind, nbytes, a, b in self.pending:
+            d = out.setdefault(kind, {"launches": 0, "bytes": 0, "seconds": 0.0})
+            d["launches"] += 1
+            d["bytes"] += nbytes
+            d["seconds"] += a.elapsed_time(b) * 1e-3
+        return out
+
+
+TIMER = None  # set to a KernelTimer to time every launch
+
+
 def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
@@ -47,19 +76,6 @@ def matrix_tmap(t: torch.Tensor, box_rows: int) -> TensorMap:
     return TensorMap(t, t.shape[1], t.shape[0], t.stride(0) * 2, BK, box_rows)
 
 
-def choose_splits(n_out: int, k: int, sms: int = SMS) -> int:
-    """Fixed K-split of a projection, a function of its shape only (never of
-    the micro-batch size) so results are batch-invariant.  Minimises
-    waves x (k-blocks per CTA + fixed per-CTA overhead)."""
-    tiles, kb = n_out // BM, k // BK
-    best = (math.inf, 1)
-    for s in range(1, min(16, max(1, kb // 4)) + 1):
-        cost = math.ceil(tiles * s / sms) * (kb / s + 6.0)
-        if cost < best[0] - 1e-9:
-            best = (cost, s)
-    return best[1]
-
-
 def bn_for(m_tok: int) -> int:
     for bn in (16, 32, 64, 128, 256):
         if m_tok <= bn:
@@ -68,41 +84,93 @@ def bn_for(m_tok: int) -> int:
 
 
 EPI_STORE_BF16, EPI_RESID_ADD, EPI_SILU_MUL, EPI_LOGITS_ARGMAX = 0, 1, 2, 3
+UNIT_ROWS = 256
+
+
+def pack_weight(w: torch.Tensor):
+    """[N, K] bf16 (K-major) -> [N_pad/256][K/64][2][128][64] with every
+    128x64 tile in the 128B-swizzled K-major UMMA shared-memory image
+    (16-byte chunk c of row r stored at chunk c ^ (r % 8)), so the GEMM moves
+    one contiguous 32 KB chunk per pipeline stage with a plain bulk copy.
+    Rows are zero-padded to a multiple of 256."""
+    n, k = w.shape
+    assert k % BK == 0
+    n_pad = -(-n // UNIT_ROWS) * UNIT_ROWS
+    if n_pad != n:
+        w = torch.cat([w, torch.zeros(n_pad - n, k, dtype=w.dtype, device=w.device)])
+    kb = k // BK
+    src = w.view(n_pad // UNIT_ROWS, 2, 128, kb, 8, 8).permute(0, 3, 1, 2, 4, 5)  # unit,kb,half,row,chunk,e
+    out = torch.empty(n_pad // UNIT_ROWS, kb, 2, 128, 8, 8, dtype=w.dtype, device=w.device)
+    for rr in range(8):
+        perm = torch.tensor([c ^ rr for c in range(8)], device=w.device)
+        out[:, :, :, rr::8] = src[:, :, :, rr::8].index_select(4, perm)
+    return out, n_pad // UNIT_ROWS
+
+
+def gemm_plan(n_units: int, kb: int, m_tok: int, sms: int = SMS):
+    """Stream-K geometry of one launch: (bn, grid, max segments per unit).
+    The k-block ranges depend on (units, K, #SMs) only -- not on m_tok for
+    m_tok <= 256 -- which keeps results batch-invariant."""
+    bn = bn_for(m_tok)
+    tt = -(-m_tok // bn)
+    total = n_units * tt * kb
+    grid = min(sms, total)
+    segs = _C.lib().pm_gemm_max_segments(total, kb, grid)
+    return bn, grid, segs, tt
 
 
 class GemmWorkspace:
-    """Split-K partials, per-tile counters and argmax partials shared by all
-    projections of one executor (ops on one stream run in order)."""
+    """Stream-K partials, per-unit counters and argmax partials shared by all
+    projections of one executor (launches on one stream run in order)."""
 
-    def __init__(self, m_cap: int, max_n_out: int, max_splits: int, vocab_tiles: int, device):
+    def __init__(self, m_cap: int, ws_floats: int, max_units: int, vocab_units: int, device):
         self.m_cap = m_cap
-        self.ws = torch.empty(max_splits * m_cap * max_n_out, dtype=torch.float32, device=device)
-        tok_tiles = max(1, math.ceil(m_cap / 256))
-        self.counters = torch.zeros(tok_tiles * max(vocab_tiles, max_n_out // BM), dtype=torch.int32, device=device)
-        self.amax_val = torch.empty(max(1, vocab_tiles) * m_cap, dtype=torch.float32, device=device)
-        self.amax_idx = torch.empty(max(1, vocab_tiles) * m_cap, dtype=torch.int32, device=device)
+        self.ws = torch.empty(max(1, ws_floats), dtype=torch.float32, device=device)
+        self.amax_val = torch.empty(max(1, vocab_units) * m_cap, dtype=torch.float32, device=device)
+        self.amax_idx = torch.empty(max(1, vocab_units) * m_cap, dtype=torch.int32, device=device)
+
+    @staticmethod
+    def floats_needed(linears, m_cap):
+        need = 1
+        for lin in linears:
+            for m in sorted({min(m_cap, x) for x in (16, 32, 64, 128, 256, m_cap)}):
+                bn, grid, segs, tt = gemm_plan(lin.n_units, lin.kb, m)
+                need = max(need, lin.n_units * tt * segs * bn * UNIT_ROWS)
+        return need
 
 
 class Linear:
-    """One projection: weight [n_out, K] bf16 (K-major) + its TMA map + fixed split."""
+    """One projection: packed weight + stream-K launch plans."""
 
-    def __init__(self, weight: torch.Tensor, splits: int = None):
+    def __init__(self, weight: torch.Tensor):
         assert weight.is_contiguous() and weight.dtype == torch.bfloat16
-        self.w = weight
         self.n_out, self.k = weight.shape
-        assert self.n_out % BM == 0 and self.k % BK == 0, (self.n_out, self.k)
-        self.tmap = matrix_tmap(weight, BM)
-        self.splits = splits or choose_splits(self.n_out, self.k)
+        self.kb = self.k // BK
+        self.packed, self.n_units = pack_weight(weight)
+        self.weight_bytes = self.n_out * self.k * 2
+        self._plans = {}
+
+    def plan(self, m_tok):
+        p = self._plans.get(m_tok)
+        if p is None:
+            p = self._plans[m_tok] = gemm_plan(self.n_units, self.kb, m_tok)
+        return p
 
     def __call__(self, x_maps: dict, m_tok: int, epilogue: int, out, ld_out: int, ws: GemmWorkspace,
-                 stream=None, splits: int = None):
-        bn = bn_for(m_tok)
-        s = splits or self.splits
-        if epilogue == EPI_LOGITS_ARGMAX:
-            s = 1
-        _C.call("pm_gemm", self.tmap.ptr, x_maps[bn].ptr, self.n_out, self.k, m_tok, bn, s, epilogue,
-                _ptr(out), ld_out, _ptr(ws.ws), ws.m_cap, _ptr(ws.counters), _ptr(ws.amax_val),
-                _ptr(ws.amax_idx), _stream(stream))
+                 stream=None):
+        bn, grid, segs, tt = self.plan(m_tok)
+
+        def go():
+            _C.call("pm_gemm", _ptr(self.packed), x_maps[bn].ptr, self.n_out, self.n_units, self.k, m_tok, bn,
+                    grid, epilogue, _ptr(out), ld_out, _ptr(ws.ws), segs,
+                    _ptr(ws.amax_val), _ptr(ws.amax_idx), ws.m_cap, _stream(stream))
+        if TIMER is None:
+            go()
+        else:
+            out_b = {EPI_STORE_BF16: 2, EPI_RESID_ADD: 8, EPI_SILU_MUL: 1,
+                     EPI_LOGITS_ARGMAX: 4 if out is not None else 0}[epilogue]
+            nbytes = self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * out_b
+            TIMER.around("gemm", nbytes, stream, go)
 
 
 def activation_maps(buf: torch.Tensor) -> dict:
@@ -138,12 +206,18 @@ def attn_blocks_per_split() -> int:
 
 
 def paged_attention(tmap_kv, q, block_table, seq_lens, out, ws_o, ws_ml, counters, M, H, Hkv, hd, layer,
-                    L_s, max_splits, stream=None):
-    _C.call("pm_paged_attention", tmap_kv.ptr, _ptr(q), _ptr(block_table), _ptr(seq_lens), _ptr(out),
-            _ptr(ws_o), _ptr(ws_ml), _ptr(counters), M, H, Hkv, hd, layer, L_s, block_table.shape[1],
-            max_splits, _stream(stream))
+                    L_s, max_splits, stream=None, kv_tokens=0):
+    """``kv_tokens`` (sum of seq_lens, host-known) only feeds the optional timer."""
+    def go():
+        _C.call("pm_paged_attention", tmap_kv.ptr, _ptr(q), _ptr(block_table), _ptr(seq_lens), _ptr(out),
+                _ptr(ws_o), _ptr(ws_ml), _ptr(counters), M, H, Hkv, hd, layer, L_s, block_table.shape[1],
+                max_splits, _stream(stream))
+    if TIMER is None:
+        go()
+    else:
+        TIMER.around("attention", kv_tokens * 2 * Hkv * hd * 2 + 2 * M * H * hd * 2, stream, go)
 
 
-def argmax_reduce(ws: GemmWorkspace, n_tiles, M, out_ids, tok_table=None, slots=None, stream=None):
-    _C.call("pm_argmax_reduce", _ptr(ws.amax_val), _ptr(ws.amax_idx), n_tiles, M, ws.m_cap, _ptr(out_ids),
+def argmax_reduce(ws: GemmWorkspace, n_units, M, out_ids, tok_table=None, slots=None, stream=None):
+    _C.call("pm_argmax_reduce", _ptr(ws.amax_val), _ptr(ws.amax_idx), n_units, M, ws.m_cap, _ptr(out_ids),
             _ptr(tok_table), _ptr(slots), _stream(stream))

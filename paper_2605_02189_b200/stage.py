@@ -57,6 +57,7 @@ class StageExecutor:
         head = init_head(s, device, seed) if last else None
         self.final_norm = head["final_norm"] if last else None
         self.lm_head = ops.Linear(head["lm_head"]) if last else None
+        self.lm_head_logical = head["lm_head"] if (last and keep_logical) else None
         self.rope = torch.from_numpy(rope_table(s, max_pos)).to(device)
 
         f32, b16, i32 = torch.float32, torch.bfloat16, torch.int32
@@ -86,14 +87,13 @@ class StageExecutor:
         self.out_ids = torch.zeros(m_cap, dtype=i32, device=device)
         self.logits = None
         # workspaces
-        max_n = max([s.qkv_out, s.d, 2 * s.ffn] + ([s.vocab] if last else []))
         self.max_splits_attn = max(1, math.ceil(max_blocks / ops.attn_blocks_per_split()))
-        self.gws = ops.GemmWorkspace(m_cap, max(s.qkv_out, s.d, 2 * s.ffn), 16,
-                                     (s.vocab // ops.BM) if last else 1, device)
+        lins = [x[k] for x in self.W for k in ("qkv", "o", "gu", "down")] + ([self.lm_head] if last else [])
+        self.gws = ops.GemmWorkspace(m_cap, ops.GemmWorkspace.floats_needed(lins, m_cap),
+                                     max(l.n_units for l in lins), self.lm_head.n_units if last else 1, device)
         self.ws_o = torch.empty(m_cap * s.H * self.max_splits_attn * s.hd, dtype=f32, device=device)
         self.ws_ml = torch.empty(m_cap * s.H * self.max_splits_attn * 2, dtype=f32, device=device)
         self.attn_ctr = torch.zeros(m_cap * s.Hkv, dtype=i32, device=device)
-        del max_n
 
     # ------------------------------------------------------------------ views
     def pool_view(self):
@@ -105,7 +105,7 @@ class StageExecutor:
             self.logits = torch.zeros(self.m_cap, self.spec.vocab, dtype=torch.float32, device=self.dev)
 
     # ------------------------------------------------------------------ forward
-    def forward(self, M: int, stream=None, kernel_log=None):
+    def forward(self, M: int, stream=None, kv_tokens: int = 0):
         """One micro-batch step of M rows (metadata already on the device).
 
         Stage 0 embeds ``tok_table[slots]``; later stages expect ``resid`` to
@@ -123,7 +123,7 @@ class StageExecutor:
                                 w["q_norm"], w["k_norm"], M, s.H, s.Hkv, s.hd, li, self.L_s, s.eps, stream)
             ops.paged_attention(self.pool_map, self.q, self.block_table, self.seq_lens, self.attn, self.ws_o,
                                 self.ws_ml, self.attn_ctr, M, s.H, s.Hkv, s.hd, li, self.L_s,
-                                self.max_splits_attn, stream)
+                                self.max_splits_attn, stream, kv_tokens=kv_tokens)
             w["o"](self.attn_maps, M, ops.EPI_RESID_ADD, self.resid, s.d, self.gws, stream)
             ops.rmsnorm(self.resid, w["mlp_norm"], self.xn, M, s.eps, stream)
             w["gu"](self.xn_maps, M, ops.EPI_SILU_MUL, self.act, s.ffn, self.gws, stream)
@@ -131,7 +131,7 @@ class StageExecutor:
         if self.last:
             ops.rmsnorm(self.resid, self.final_norm, self.xn, M, s.eps, stream)
             self.lm_head(self.xn_maps, M, ops.EPI_LOGITS_ARGMAX, self.logits, s.vocab, self.gws, stream)
-            ops.argmax_reduce(self.gws, s.vocab // ops.BM, M, self.out_ids, self.tok_table, self.slots, stream)
+            ops.argmax_reduce(self.gws, self.lm_head.n_units, M, self.out_ids, self.tok_table, self.slots, stream)
 
     def kernels_per_step(self) -> int:
         return (1 if self.first else 0) + 8 * self.L_s + (3 if self.last else 0)
@@ -141,10 +141,10 @@ class StageExecutor:
         """Algorithmic HBM bytes of one step: weights once, the micro-batch's
         KV once per layer, new KV written once, activations (stated, small)."""
         s = self.spec
-        w = sum(x["qkv"].w.numel() + x["o"].w.numel() + x["gu"].w.numel() + x["down"].w.numel()
-                for x in self.W) * 2
+        w = sum(x["qkv"].weight_bytes + x["o"].weight_bytes + x["gu"].weight_bytes + x["down"].weight_bytes
+                for x in self.W)
         if self.last:
-            w += self.lm_head.w.numel() * 2
+            w += self.lm_head.weight_bytes
         kv = (kv_tokens + M) * self.tok_bytes
         act = self.L_s * M * (4 * s.d * 4 + 2 * (s.qkv_out + 2 * s.H * s.hd + s.ffn)) * 1
         return w + kv + act

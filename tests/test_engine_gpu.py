@@ -54,7 +54,7 @@ def oracle_model(eng, storage_bf16=False):
     hp = dict(d=spec.d, layers=spec.layers, H=spec.H, Hkv=spec.Hkv, hd=spec.hd, ffn=spec.ffn,
               vocab=spec.vocab, qk_norm=spec.qk_norm, eps=spec.eps)
     return RefModel(hp, layers, ex0.embed.float().cpu().numpy(), exl.final_norm.float().cpu().numpy(),
-                    exl.lm_head.w.float().cpu().numpy(), rope_table(spec, eng.max_pos),
+                    exl.lm_head_logical.float().cpu().numpy(), rope_table(spec, eng.max_pos),
                     storage_bf16=storage_bf16)
 
 

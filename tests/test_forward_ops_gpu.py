@@ -62,7 +62,7 @@ def test_single_token_stage_forward(spec, pos):
         h = R(ref.rmsnorm(x, L["mlp_norm"], s.eps))
         x = x + L["w_down"] @ R(ref.silu(L["w_gate"] @ h) * (L["w_up"] @ h))
     h = R(ref.rmsnorm(x, ex.final_norm.float().cpu().numpy(), s.eps))
-    want = ex.lm_head.w.float().cpu().numpy() @ h
+    want = ex.lm_head_logical.float().cpu().numpy() @ h
     got = ex.logits[0].cpu().numpy()
     scale = np.abs(want).max()
     err = np.abs(got - want).max()

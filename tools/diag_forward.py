@@ -71,5 +71,5 @@ ops.rmsnorm(ex.resid, ex.final_norm, ex.xn, M, s.eps)
 h = R(ref.rmsnorm(x, ex.final_norm.float().cpu().numpy(), s.eps))
 cmp("final xn", ex.xn[0], h)
 ex.lm_head(ex.xn_maps, M, ops.EPI_LOGITS_ARGMAX, ex.logits, s.vocab, ex.gws)
-cmp("logits", ex.logits[0], ex.lm_head.w.float().cpu().numpy() @ h)
+cmp("logits", ex.logits[0], ex.lm_head_logical.float().cpu().numpy() @ h)
 torch.cuda.synchronize()
