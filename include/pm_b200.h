@@ -54,6 +54,9 @@ int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_tabl
                        void* out, float* ws_o, float* ws_ml, int* counters, int M, int H, int Hkv, int hd,
                        int layer, int L_s, int max_blocks, int max_splits, void* stream);
 int pm_attn_blocks_per_split(void);
+/* one-time kernel attributes; call once per device before CUDA-graph capture */
+int pm_prepare_gemm(void);
+int pm_prepare_attention(void);
 int pm_argmax_reduce(const float* val, const int* idx, int n_tiles, int M, int m_cap, int* out_ids,
                      int* tok_table, const int* slots, void* stream);
 

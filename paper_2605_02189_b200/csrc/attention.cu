@@ -289,3 +289,12 @@ extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int*
 }
 
 extern "C" int pm_attn_blocks_per_split(void) { return BLOCKS_PER_SPLIT; }
+
+extern "C" int pm_prepare_attention(void) {
+  constexpr int S128 = WARPS * STAGES * 2 * 16 * 128 * 2 + WARPS * STAGES * 8 + 1024;
+  constexpr int S64 = WARPS * STAGES * 2 * 16 * 64 * 2 + WARPS * STAGES * 8 + 1024;
+  cudaError_t e = cudaFuncSetAttribute(paged_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, S128);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(paged_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, S64);
+  return (int)e;
+}

@@ -391,6 +391,17 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st) {
 
 }  // namespace
 
+// One-time kernel attributes (call before any CUDA-graph capture).
+extern "C" int pm_prepare_gemm(void) {
+  cudaError_t e = cudaSuccess;
+#define PM_SET(BN)                                                                                        \
+  if (e == cudaSuccess)                                                                                   \
+    e = cudaFuncSetAttribute(gemm_stream_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
+  PM_SET(16) PM_SET(32) PM_SET(64) PM_SET(128) PM_SET(256)
+#undef PM_SET
+  return (int)e;
+}
+
 // Segments a unit of `kb` k-blocks can be cut into by `grid` CTAs over `total`
 // k-blocks (host helper for workspace sizing; mirrors owner_of()).
 extern "C" int pm_gemm_max_segments(long long total, int kb, int grid) {

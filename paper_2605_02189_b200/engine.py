@@ -60,7 +60,7 @@ class DecodeEngine:
     def __init__(self, spec: ModelSpec, state: SchedulerState, cfg: ClusterConfig, params: EstimatorParams,
                  requests: dict, *, pp: int = 1, device="cuda", mode="dynamic", quota_tokens=0,
                  seed: int = 0, m_cap: int = None, timing=True, kv_init="random", prompts=None,
-                 record_logits=False, max_pos=None, trace: EventTrace = None):
+                 record_logits=False, max_pos=None, trace: EventTrace = None, graphs: bool = True):
         self.spec, self.cfg, self.params = spec, cfg, params
         self.requests = requests
         self.dev = torch.device(device)
@@ -76,12 +76,17 @@ class DecodeEngine:
         self.max_blocks = blocks_for_tokens(max_len + 1, bs)
         self.m_cap = m_cap or len(rids)
         self.max_pos = max_pos or (self.max_blocks * bs)
-        pool_blocks = self.control.alloc.total
+        # +1 physical block and +1 token slot: padding rows of a bucketed
+        # micro-batch point there, so CUDA graphs are captured per 16-row bucket
+        pool_blocks = self.control.alloc.total + 1
+        self.trash_block = self.control.alloc.total
+        self.trash_slot = len(rids)
+        self.graphs = graphs
         self.stages = []
         for s in range(pp):
             ex = StageExecutor(spec, stage_layers(spec, pp, s), first=(s == 0), last=(s == pp - 1),
                                m_cap=self.m_cap, pool_blocks=pool_blocks, max_blocks=self.max_blocks,
-                               n_slots=len(rids), device=self.dev, seed=seed, max_pos=self.max_pos,
+                               n_slots=len(rids) + 1, device=self.dev, seed=seed, max_pos=self.max_pos,
                                keep_logical=record_logits)
             if record_logits:
                 ex.enable_logits()
@@ -93,6 +98,10 @@ class DecodeEngine:
         self.ids_log = []      # (t, rows, ids np)
         self.t = 0
         self.n_evicted = self.n_prefetched = 0
+        if graphs:  # one graph per 16-row bucket, captured up front
+            for ex, kv in self.stages:
+                for Mb in range(16, self.m_cap + 16, 16):
+                    ex.capture(min(Mb, self.m_cap), kv.compute)
         self._init_kv(kv_init, prompts, seed)
 
     # ------------------------------------------------------------------ setup
@@ -102,7 +111,7 @@ class DecodeEngine:
         bulk load, pipeline_sim.py:732-739)."""
         rids = sorted(self.requests)
         g = torch.Generator(device=self.dev).manual_seed(seed + 1)
-        first_tok = torch.randint(0, self.spec.vocab, (len(rids),), generator=g, device=self.dev,
+        first_tok = torch.randint(0, self.spec.vocab, (len(rids) + 1,), generator=g, device=self.dev,
                                   dtype=torch.int32)
         for ex, kv in self.stages:
             if ex.first:
@@ -179,8 +188,14 @@ class DecodeEngine:
         torch.cuda.synchronize()
 
     # ------------------------------------------------------------------ per step
+    def bucket(self, M):
+        return min(self.m_cap, -(-M // 16) * 16) if self.graphs else M
+
     def _upload_meta(self, rows, positions, tables, stream=None):
-        M, mb = len(rows), self.max_blocks
+        """Block tables, positions, seq lens and slots of the step's rows,
+        padded to the 16-row bucket with rows aimed at the trash block/slot."""
+        n, mb = len(rows), self.max_blocks
+        M = self.bucket(n)
         k, buf = self.meta.next()
         a = buf.numpy()
         bt = a[:M * mb].reshape(M, mb)
@@ -188,10 +203,14 @@ class DecodeEngine:
         for i, r in enumerate(rows):
             tb = tables[r]
             bt[i, :len(tb)] = tb
+        bt[n:, 0] = self.trash_block
         o = M * mb
-        a[o:o + M] = positions
-        a[o + M:o + 2 * M] = np.asarray(positions) + 1
-        a[o + 2 * M:o + 3 * M] = [self.slot_of[r] for r in rows]
+        a[o:o + n] = positions
+        a[o + n:o + M] = 0
+        a[o + M:o + M + n] = np.asarray(positions) + 1
+        a[o + M + n:o + 2 * M] = 1
+        a[o + 2 * M:o + 2 * M + n] = [self.slot_of[r] for r in rows]
+        a[o + 2 * M + n:o + 3 * M] = self.trash_slot
         evs = []
         for ex, kv in self.stages:
             s = kv.compute if stream is None else stream
@@ -205,9 +224,10 @@ class DecodeEngine:
             evs.append(ev)
         self.meta.events[k] = evs
 
-    def _forward_all(self, M, kv_tokens=0):
+    def _forward_all(self, n, kv_tokens=0):
         """Run the stages in order on their compute streams (single process:
         stage s+1 waits for stage s's activations via an event)."""
+        M = self.bucket(n)
         prev_ev = None
         for si, (ex, kv) in enumerate(self.stages):
             if prev_ev is not None:
@@ -215,7 +235,7 @@ class DecodeEngine:
             with torch.cuda.stream(kv.compute):
                 if si > 0:
                     ex.resid[:M].copy_(self.stages[si - 1][0].resid[:M])
-                ex.forward(M, kv.compute, kv_tokens=kv_tokens)
+                ex.run(M, kv.compute, graphs=self.graphs, kv_tokens=kv_tokens)
                 if si == len(self.stages) - 1 and len(self.stages) > 1:
                     # greedy ids back to stage 0's token table (the last->first hop)
                     first = self.stages[0][0]

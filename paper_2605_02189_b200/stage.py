@@ -19,7 +19,7 @@ import math
 
 import torch
 
-from . import ops
+from . import _C, ops
 from .models import ModelSpec, init_embed, init_head, init_layer_weights, rope_table
 
 
@@ -86,6 +86,9 @@ class StageExecutor:
         self.tok_table = torch.zeros(n_slots, dtype=i32, device=device)
         self.out_ids = torch.zeros(m_cap, dtype=i32, device=device)
         self.logits = None
+        self.graphs = {}
+        _C.call("pm_prepare_gemm")
+        _C.call("pm_prepare_attention")
         # workspaces
         self.max_splits_attn = max(1, math.ceil(max_blocks / ops.attn_blocks_per_split()))
         lins = [x[k] for x in self.W for k in ("qkv", "o", "gu", "down")] + ([self.lm_head] if last else [])
@@ -132,6 +135,27 @@ class StageExecutor:
             ops.rmsnorm(self.resid, self.final_norm, self.xn, M, s.eps, stream)
             self.lm_head(self.xn_maps, M, ops.EPI_LOGITS_ARGMAX, self.logits, s.vocab, self.gws, stream)
             ops.argmax_reduce(self.gws, self.lm_head.n_units, M, self.out_ids, self.tok_table, self.slots, stream)
+
+    def run(self, M: int, stream, graphs: bool = True, kv_tokens: int = 0):
+        """forward(M) on ``stream``; with ``graphs`` the whole kernel sequence
+        for this M is captured once into a CUDA graph and replayed (the step's
+        metadata lives in fixed device buffers, so replays see new rows)."""
+        if not graphs or ops.TIMER is not None:
+            self.forward(M, stream, kv_tokens=kv_tokens)
+            return
+        g = self.graphs.get(M)
+        if g is None:
+            g = self.capture(M, stream)
+        with torch.cuda.stream(stream):
+            g.replay()
+
+    def capture(self, M: int, stream):
+        """Record forward(M) into a CUDA graph (capture launches nothing)."""
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            self.forward(M, stream)
+        self.graphs[M] = g
+        return g
 
     def kernels_per_step(self) -> int:
         return (1 if self.first else 0) + 8 * self.L_s + (3 if self.last else 0)

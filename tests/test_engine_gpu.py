@@ -27,7 +27,7 @@ def _cap_cfg(n, cap_blocks, kv_bytes):
                          h2d_bandwidth=55e9, d2h_bandwidth=55e9, cpu_kv_capacity=10**15, block_size=16)
 
 
-def build(n_req=24, m=4, cap=40, seed=3, pp=1):
+def build(n_req=24, m=4, cap=40, seed=3, pp=1, graphs=True):
     rng = np.random.default_rng(seed)
     spec = TINY
     reqs = {i: Request(i, int(rng.integers(17, 41)), int(rng.integers(6, 16))) for i in range(n_req)}
@@ -40,7 +40,7 @@ def build(n_req=24, m=4, cap=40, seed=3, pp=1):
     cfg = _cap_cfg(m, cap, spec.kv_bytes_per_token())
     params = EstimatorParams(1e-6, 2e-8, 1e-4)
     eng = DecodeEngine(spec, st, cfg, params, reqs, pp=pp, kv_init="prefill", prompts=prompts,
-                       record_logits=True, seed=seed)
+                       record_logits=True, seed=seed, graphs=graphs)
     return spec, eng, reqs, prompts
 
 
@@ -58,9 +58,9 @@ def oracle_model(eng, storage_bf16=False):
                     storage_bf16=storage_bf16)
 
 
-@pytest.mark.parametrize("pp", [1, 2])
-def test_engine_matches_oracle_with_offload(pp):
-    spec, eng, reqs, prompts = build(pp=pp)
+@pytest.mark.parametrize("pp,graphs", [(1, True), (2, False)])
+def test_engine_matches_oracle_with_offload(pp, graphs):
+    spec, eng, reqs, prompts = build(pp=pp, graphs=graphs)
     first_tok = eng.stages[0][0].tok_table.cpu().numpy().copy()
     n = eng.run(horizon=25)
     check_replica(eng)
