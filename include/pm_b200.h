@@ -52,7 +52,7 @@ int pm_qkv_rope_append(const void* qkv, void* q_out, void* pool, const int* bloc
                        int layer, int L_s, int max_blocks, float eps, void* stream);
 int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_table, const int* seq_lens,
                        void* out, float* ws_o, float* ws_ml, int* counters, int M, int H, int Hkv, int hd,
-                       int layer, int L_s, int max_blocks, int max_splits, void* stream);
+                       int layer, int L_s, int max_blocks, int max_chunks, int blocks_per_chunk, void* stream);
 int pm_attn_blocks_per_split(void);
 /* one-time kernel attributes; call once per device before CUDA-graph capture */
 int pm_prepare_gemm(void);

@@ -1,27 +1,31 @@
 // Paged GQA decode attention over the block-first KV pool (one query token
 // per request).  HBM-bound: every KV byte of the active micro-batch is read
-// once per layer.
+// exactly once per layer, so the kernel is built to keep every SM streaming.
 //
-// CTA = (request row, kv head, split of 16 KV blocks); 4 warps, each warp
-// owns every 4th block of the split and runs its own 2-stage TMA pipeline:
-// one lane issues the 128B-swizzled TMA boxes of a [16 tok x hd] K tile and
-// V tile, the warp consumes them with ldmatrix + mma.sync.m16n8k16 in the
-// "transposed" arrangement
-//     S^T[16 tok x 8 heads] = K[16 x hd] . Q^T[hd x 8]
-//     O^T[hd x 8 heads]   += V^T[hd x 16] . P^T[16 x 8]
-// so the 8 q-heads of a GQA group fill the MMA N=8 exactly (Qwen3-32B,
-// Llama-70B; half-filled for group 4) and P^T goes from the S accumulator to
-// the B fragment with one movmatrix.trans per 8x8.  Online softmax in fp32
-// with warp shuffles; warps merge in shared memory; splits merge in the last
-// CTA of a (request, kv head) in split order, so results depend only on the
-// request's own length (batch-invariant).
+// Work item = (request row, kv head, chunk of `bpc` 16-token KV blocks).
+// Persistent grid; every WARP is an independent worker that walks its share
+// of the items with its own STAGES-deep TMA pipeline that runs straight
+// across item boundaries (no CTA-wide barriers on the hot path):
+//   lane 0 issues, per KV block, four 128B-swizzled 2-D TMA boxes (K and V,
+//   two 64-dim halves each) and, for the first block of an item, a bulk copy
+//   of the item's GQA query group; the warp consumes them with ldmatrix +
+//   mma.sync.m16n8k16 in the transposed arrangement
+//       S^T[16 tok x 8 heads] = K[16 x hd] . Q^T[hd x 8]
+//       O^T[hd x 8 heads]   += V^T[hd x 16] . P^T[16 x 8]
+//   (the 8 q-heads of a GQA group are the MMA N; P^T moves from the S
+//   accumulator to the B fragment with one movmatrix.trans per 8x8), online
+//   softmax in fp32 with warp shuffles.
+// A request with one chunk is normalised and stored by its warp; otherwise
+// chunk partials (O, m, l) go to a workspace and the last warp to finish a
+// (request, kv head) merges them in chunk order -- chunk boundaries depend
+// only on the request's own length, so results are batch-invariant.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace {
 
-constexpr int BLOCKS_PER_SPLIT = 16;
-constexpr int WARPS = 4;
-constexpr int STAGES = 2;
+constexpr int MAX_G = 8;
 
 PM_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -42,6 +46,10 @@ PM_DEV void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+PM_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 // byte offset of 16-byte chunk `chunk` (0..7) of row `row` in a 128B-swizzled [rows][128 B] tile
 PM_DEV uint32_t sw128(int row, int chunk) { return row * 128 + ((chunk ^ (row & 7)) << 4); }
 
@@ -50,99 +58,175 @@ struct AttnArgs {
   const int* block_table;  // [M][max_blocks]
   const int* seq_lens;     // [M]
   bf16* out;               // [M][H][HD]
-  float* ws_o;             // [M][H][max_splits][HD]
-  float* ws_ml;            // [M][H][max_splits][2]
+  float* ws_o;             // [M][Hkv][max_chunks][8][HD]
+  float* ws_ml;            // [M][Hkv][max_chunks][2][8]
   int* counters;           // [M][Hkv] zero at rest
-  int H, Hkv, G, layer, L_s, max_blocks, max_splits;
+  int M, H, Hkv, G, layer, max_blocks, max_chunks, bpc;
   float scale_log2;        // log2(e)/sqrt(hd)
 };
 
+// cursor over a warp's (item, block) sequence: items gw, gw+W, gw+2W, ...
+struct Cursor {
+  int item, blk, nblk, r, kvh, chunk, b0;  // b0 = first block of the chunk
+};
+
+PM_DEV bool item_setup(const AttnArgs& a, int item, Cursor& c) {
+  const int per_row = a.Hkv * a.max_chunks;
+  if (item >= a.M * per_row) return false;
+  c.item = item;
+  c.r = item / per_row;
+  const int rem = item % per_row;
+  c.kvh = rem / a.max_chunks;
+  c.chunk = rem % a.max_chunks;
+  const int nblk_total = (a.seq_lens[c.r] + 15) >> 4;
+  c.b0 = c.chunk * a.bpc;
+  c.nblk = min(a.bpc, nblk_total - c.b0);
+  c.blk = 0;
+  return true;
+}
+// advance to the first non-empty item at or after `item` (stride W)
+PM_DEV bool next_item(const AttnArgs& a, int item, int W, Cursor& c) {
+  while (item_setup(a, item, c)) {
+    if (c.nblk > 0) return true;
+    item += W;
+  }
+  return false;
+}
+
+template <int HD, int WARPS, int STAGES>
+struct AttnCfg {
+  static constexpr int TILE = 16 * HD * 2;          // one K or V tile
+  static constexpr int STAGE = 2 * TILE;
+  static constexpr int SMEM = WARPS * STAGES * STAGE + WARPS * (STAGES * 8 + 2 * 64 * 4) + 1024;
+};
+
+// Q^T fragments of an item's GQA group straight from global (prefetched one
+// item ahead): head n = lane/4 of the group, dim pairs 2t and 2t+8 per k-chunk
 template <int HD>
+PM_DEV void load_q(const AttnArgs& a, const Cursor& c, int lane, uint32_t (&q)[HD / 16][2]) {
+  const int g8 = lane >> 2, t = lane & 3;
+  const bool live = g8 < a.G;
+  const uint32_t* row = reinterpret_cast<const uint32_t*>(a.q + ((size_t)c.r * a.H + c.kvh * a.G + (live ? g8 : 0)) * HD);
+#pragma unroll
+  for (int kc = 0; kc < HD / 16; ++kc) {
+    q[kc][0] = live ? __ldg(&row[(kc * 16 + 2 * t) >> 1]) : 0u;
+    q[kc][1] = live ? __ldg(&row[(kc * 16 + 8 + 2 * t) >> 1]) : 0u;
+  }
+}
+
+template <int HD, int WARPS, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32)
 paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
-  constexpr int HALVES = HD / 64;             // 64-col TMA boxes per tile
-  constexpr int TILE = 16 * HD * 2;           // bytes of one K (or V) tile
-  constexpr int STAGE = 2 * TILE;             // K + V
-  constexpr int KC = HD / 16;                 // k-chunks of QK, m-tiles of PV
+  using C = AttnCfg<HD, WARPS, STAGES>;
+  constexpr int HALVES = HD / 64;
+  constexpr int KC = HD / 16;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* wbuf = smem + warp * STAGES * STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * STAGE) + warp * STAGES;
-  float* mrg = reinterpret_cast<float*>(smem);  // reused after the main loop: [WARPS][8][HD] + m,l
-  __shared__ int s_last;
+  uint8_t* wbuf = smem + warp * STAGES * C::STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * C::STAGE) + warp * STAGES;
+  // physical block ids of the producer's current item, staged once per item (2 slots by parity)
+  int* bids = reinterpret_cast<int*>(smem + WARPS * STAGES * C::STAGE + WARPS * STAGES * 8) + warp * 2 * 64;
+  const int W = gridDim.x * WARPS;
+  const int gw = blockIdx.x * WARPS + warp;
+  const int G = a.G;
 
-  const int r = blockIdx.x, kvh = blockIdx.y, split = blockIdx.z;
-  const int seq = a.seq_lens[r];
-  const int nblk = (seq + 15) >> 4;
-  const int nsplit = (nblk + BLOCKS_PER_SPLIT - 1) / BLOCKS_PER_SPLIT;
-  if (split >= nsplit) return;
-  const int b_begin = split * BLOCKS_PER_SPLIT;
-  const int b_end = min(nblk, b_begin + BLOCKS_PER_SPLIT);
-  const int my_n = b_end - b_begin > warp ? (b_end - b_begin - warp + WARPS - 1) / WARPS : 0;
-  const int* btab = a.block_table + (size_t)r * a.max_blocks;
-  const int col_k = ((a.layer * 2 + 0) * a.Hkv + kvh) * HD;
-  const int col_v = ((a.layer * 2 + 1) * a.Hkv + kvh) * HD;
-
+  pdl_trigger();
   if (lane == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
   }
   __syncwarp();
-  auto issue = [&](int i) {  // lane 0 only
-    const int s = i % STAGES;
-    const int phys = btab[b_begin + warp + i * WARPS];
+  pdl_wait();  // q and the appended KV come from the previous kernel
+
+  // producer cursor (lane 0 issues STAGES blocks ahead of the consumer)
+  Cursor pc;
+  bool p_live = next_item(a, gw, W, pc);
+  int issued = 0, p_items = 0;
+  auto stage_ids = [&]() {  // lane 0: this item's block ids -> smem slot (p_items & 1)
+    int* dst = bids + (p_items & 1) * 64;
+    const int* src = a.block_table + (size_t)pc.r * a.max_blocks + pc.b0;
+    for (int k = 0; k < pc.nblk; ++k) dst[k] = src[k];
+  };
+  if (lane == 0 && p_live) stage_ids();
+  auto issue_one = [&]() {  // lane 0
+    const int s = issued % STAGES;
+    uint8_t* dst = wbuf + s * C::STAGE;
+    const int phys = bids[(p_items & 1) * 64 + pc.blk];
+    const int col_k = ((a.layer * 2 + 0) * a.Hkv + pc.kvh) * HD;
+    const int col_v = ((a.layer * 2 + 1) * a.Hkv + pc.kvh) * HD;
     const uint64_t pol = policy_evict_first();
-    mbar_arrive_expect_tx(&bars[s], STAGE);
-    uint8_t* dst = wbuf + s * STAGE;
+    mbar_arrive_expect_tx(&bars[s], 2 * C::TILE);
 #pragma unroll
     for (int hh = 0; hh < HALVES; ++hh) {
       tma_load_2d(dst + hh * 2048, &tmap_kv, &bars[s], col_k + hh * 64, phys * 16, pol);
-      tma_load_2d(dst + TILE + hh * 2048, &tmap_kv, &bars[s], col_v + hh * 64, phys * 16, pol);
+      tma_load_2d(dst + C::TILE + hh * 2048, &tmap_kv, &bars[s], col_v + hh * 64, phys * 16, pol);
+    }
+    ++issued;
+    if (++pc.blk == pc.nblk) {
+      p_live = next_item(a, pc.item + W, W, pc);
+      ++p_items;
+      if (p_live) stage_ids();
     }
   };
   if (lane == 0) {
-    for (int i = 0; i < STAGES && i < my_n; ++i) issue(i);
+    for (int k = 0; k < STAGES && p_live; ++k) issue_one();
   }
 
-  // Q^T fragments (B operand): head n = lane/4 of the group, d pairs 2t, 2t+8
-  const int g = lane >> 2, t = lane & 3;
-  uint32_t qf[KC][2];
+  const int g8 = lane >> 2, t = lane & 3;
+  // per-lane ldmatrix offsets inside a (swizzled) K tile and V tile
+  uint32_t koff[KC], voff[KC];
   {
-    const bool live = g < a.G;
-    const uint32_t* qrow = reinterpret_cast<const uint32_t*>(a.q + ((size_t)r * a.H + kvh * a.G + (live ? g : 0)) * HD);
+    const int krow = ((lane >> 3) & 1) * 8 + (lane & 7);
+    const int q4 = lane >> 3, vtok = (q4 >> 1) * 8 + (lane & 7);
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
-      qf[kc][0] = live ? qrow[(kc * 16 + 2 * t) >> 1] : 0u;
-      qf[kc][1] = live ? qrow[(kc * 16 + 8 + 2 * t) >> 1] : 0u;
+      const int dk = kc * 16 + (lane >> 4) * 8;
+      koff[kc] = (dk >> 6) * 2048 + sw128(krow, (dk & 63) >> 3);
+      const int dv = kc * 16 + (q4 & 1) * 8;
+      voff[kc] = C::TILE + (dv >> 6) * 2048 + sw128(vtok, (dv & 63) >> 3);
     }
   }
+  Cursor cc, cn;
+  bool c_live = next_item(a, gw, W, cc), n_live = false;
+  int consumed = 0;
+  uint32_t qf[KC][2], qn[KC][2];
+  if (c_live) load_q<HD>(a, cc, lane, qn);
   float o[KC][4];
+  float mrun[2], lrun[2];
+  while (c_live) {
+    if (cc.blk == 0) {
+      // new item: take the prefetched Q^T, prefetch the next item's, reset
 #pragma unroll
-  for (int i = 0; i < KC; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float mrun[2] = {-INFINITY, -INFINITY}, lrun[2] = {0.f, 0.f};
-
-  for (int i = 0; i < my_n; ++i) {
-    const int s = i % STAGES;
-    mbar_wait(&bars[s], (i / STAGES) & 1);
-    const uint32_t kbase = smem_u32(wbuf + s * STAGE), vbase = kbase + TILE;
+      for (int kc = 0; kc < KC; ++kc) { qf[kc][0] = qn[kc][0]; qf[kc][1] = qn[kc][1]; }
+      n_live = next_item(a, cc.item + W, W, cn);
+      if (n_live) load_q<HD>(a, cn, lane, qn);
+#pragma unroll
+      for (int i = 0; i < KC; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      mrun[0] = mrun[1] = -INFINITY;
+      lrun[0] = lrun[1] = 0.f;
+    }
+    const int s = consumed % STAGES;
+    mbar_wait(&bars[s], (consumed / STAGES) & 1);
+    const uint32_t kbase = smem_u32(wbuf + s * C::STAGE);
     // ---- S^T = K Q^T
-    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+    float sc[4] = {0.f, 0.f, 0.f, 0.f}, sd[4] = {0.f, 0.f, 0.f, 0.f};  // two chains
     {
-      const int row = ((lane >> 3) & 1) * 8 + (lane & 7);
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) {
-        const int d = kc * 16 + (lane >> 4) * 8;
         uint32_t a0, a1, a2, a3;
-        ldsm_x4(kbase + (d >> 6) * 2048 + sw128(row, (d & 63) >> 3), a0, a1, a2, a3);
-        mma16816(sc, a0, a1, a2, a3, qf[kc][0], qf[kc][1]);
+        ldsm_x4(kbase + koff[kc], a0, a1, a2, a3);
+        mma16816((kc & 1) ? sd : sc, a0, a1, a2, a3, qf[kc][0], qf[kc][1]);
       }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sc[e] += sd[e];
     }
-    // ---- mask + online softmax (columns = heads 2t, 2t+1; rows = tokens g, g+8)
-    const int tok0 = (b_begin + warp + i * WARPS) * 16;
-    const bool v0 = tok0 + g < seq, v1 = tok0 + g + 8 < seq;
-    float x0 = v0 ? sc[0] * a.scale_log2 : -INFINITY, x1 = v0 ? sc[1] * a.scale_log2 : -INFINITY;
-    float x2 = v1 ? sc[2] * a.scale_log2 : -INFINITY, x3 = v1 ? sc[3] * a.scale_log2 : -INFINITY;
+    // ---- mask + online softmax (columns = heads 2t, 2t+1; rows = tokens g8, g8+8)
+    const int seq = a.seq_lens[cc.r];
+    const int tok0 = (cc.b0 + cc.blk) * 16;
+    const bool v0 = tok0 + g8 < seq, v1 = tok0 + g8 + 8 < seq;
+    const float x0 = v0 ? sc[0] * a.scale_log2 : -INFINITY, x1 = v0 ? sc[1] * a.scale_log2 : -INFINITY;
+    const float x2 = v1 ? sc[2] * a.scale_log2 : -INFINITY, x3 = v1 ? sc[3] * a.scale_log2 : -INFINITY;
     float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
@@ -151,150 +235,190 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
     }
     const float mn0 = fmaxf(mrun[0], mx0), mn1 = fmaxf(mrun[1], mx1);
     const float al0 = exp2f(mrun[0] - mn0), al1 = exp2f(mrun[1] - mn1);
-    mrun[0] = mn0; mrun[1] = mn1;
+    mrun[0] = mn0;
+    mrun[1] = mn1;
     const float p0 = exp2f(x0 - mn0), p1 = exp2f(x1 - mn1), p2 = exp2f(x2 - mn0), p3 = exp2f(x3 - mn1);
     lrun[0] = lrun[0] * al0 + p0 + p2;
     lrun[1] = lrun[1] * al1 + p1 + p3;
+    if (__any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f)) {
 #pragma unroll
-    for (int mt = 0; mt < KC; ++mt) { o[mt][0] *= al0; o[mt][1] *= al1; o[mt][2] *= al0; o[mt][3] *= al1; }
+      for (int mt = 0; mt < KC; ++mt) { o[mt][0] *= al0; o[mt][1] *= al1; o[mt][2] *= al0; o[mt][3] *= al1; }
+    }
     const uint32_t pb0 = movmatrix_t(pack_bf16(p0, p1));  // tokens 0-7  -> b0
     const uint32_t pb1 = movmatrix_t(pack_bf16(p2, p3));  // tokens 8-15 -> b1
     // ---- O^T += V^T P^T
-    {
-      const int q4 = lane >> 3, ii = lane & 7;
-      const int tok = (q4 >> 1) * 8 + ii;
 #pragma unroll
-      for (int mt = 0; mt < KC; ++mt) {
-        const int d = mt * 16 + (q4 & 1) * 8;
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4_t(vbase + (d >> 6) * 2048 + sw128(tok, (d & 63) >> 3), a0, a1, a2, a3);
-        mma16816(o[mt], a0, a1, a2, a3, pb0, pb1);
-      }
+    for (int mt = 0; mt < KC; ++mt) {
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4_t(kbase + voff[mt], a0, a1, a2, a3);
+      mma16816(o[mt], a0, a1, a2, a3, pb0, pb1);
     }
     __syncwarp();
-    if (lane == 0 && i + STAGES < my_n) {
+    ++consumed;
+    if (lane == 0 && p_live) {
       fence_proxy_async();
-      issue(i + STAGES);
+      issue_one();  // refill the slot just consumed
     }
-  }
-  // row sums: reduce the per-lane partial l over the 8 token-lanes of a column
+    if (++cc.blk < cc.nblk) continue;
+
+    // ---- item done: per-column row sums, then store or stash the partial
+    float l0 = lrun[0], l1 = lrun[1];
 #pragma unroll
-  for (int off = 4; off < 32; off <<= 1) {
-    lrun[0] += __shfl_xor_sync(0xffffffffu, lrun[0], off);
-    lrun[1] += __shfl_xor_sync(0xffffffffu, lrun[1], off);
-  }
-  __syncthreads();  // all warps done with their stage buffers -> reuse as merge area
-  // merge area: per warp [8 heads][HD] O + [8] m + [8] l
-  float* wo = mrg + warp * (8 * HD + 16);
-#pragma unroll
-  for (int mt = 0; mt < KC; ++mt) {
-    const int d = mt * 16 + g;
-    wo[(2 * t) * HD + d] = o[mt][0];
-    wo[(2 * t + 1) * HD + d] = o[mt][1];
-    wo[(2 * t) * HD + d + 8] = o[mt][2];
-    wo[(2 * t + 1) * HD + d + 8] = o[mt][3];
-  }
-  if (g == 0) {
-    wo[8 * HD + 2 * t] = mrun[0]; wo[8 * HD + 2 * t + 1] = mrun[1];
-    wo[8 * HD + 8 + 2 * t] = lrun[0]; wo[8 * HD + 8 + 2 * t + 1] = lrun[1];
-  }
-  __syncthreads();
-  const int G = a.G;
-  const bool single = nsplit == 1;
-  // each thread handles (head, d) pairs
-  for (int e = threadIdx.x; e < G * HD; e += blockDim.x) {
-    const int h = e / HD, d = e % HD;
-    float M = -INFINITY;
-    for (int w = 0; w < WARPS; ++w) M = fmaxf(M, mrg[w * (8 * HD + 16) + 8 * HD + h]);
-    float acc = 0.f, l = 0.f;
-    for (int w = 0; w < WARPS; ++w) {
-      const float* ww = mrg + w * (8 * HD + 16);
-      const float f = ww[8 * HD + h] == -INFINITY ? 0.f : exp2f(ww[8 * HD + h] - M);
-      acc += ww[h * HD + d] * f;
-      l += ww[8 * HD + 8 + h] * f;
+    for (int off = 4; off < 32; off <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, off);
     }
-    const int head = kvh * G + h;
-    if (single) {
-      a.out[((size_t)r * a.H + head) * HD + d] = __float2bfloat16(acc / l);
+    const int r = cc.r, kvh = cc.kvh;
+    const int nchunks = (((seq + 15) >> 4) + a.bpc - 1) / a.bpc;
+    const int h0 = 2 * t, h1 = 2 * t + 1;
+    if (nchunks == 1) {
+      const float i0 = 1.f / l0, i1 = 1.f / l1;
+#pragma unroll
+      for (int mt = 0; mt < KC; ++mt) {
+        const int d = mt * 16 + g8;
+        if (h0 < G) {
+          bf16* dst = a.out + ((size_t)r * a.H + kvh * G + h0) * HD;
+          dst[d] = __float2bfloat16(o[mt][0] * i0);
+          dst[d + 8] = __float2bfloat16(o[mt][2] * i0);
+        }
+        if (h1 < G) {
+          bf16* dst = a.out + ((size_t)r * a.H + kvh * G + h1) * HD;
+          dst[d] = __float2bfloat16(o[mt][1] * i1);
+          dst[d + 8] = __float2bfloat16(o[mt][3] * i1);
+        }
+      }
     } else {
-      const size_t base = ((size_t)r * a.H + head) * a.max_splits + split;
-      a.ws_o[base * HD + d] = acc;
-      if (d == 0) { a.ws_ml[base * 2] = M; a.ws_ml[base * 2 + 1] = l; }
+      const size_t rk = (size_t)r * a.Hkv + kvh;
+      float* wo = a.ws_o + (rk * a.max_chunks + cc.chunk) * MAX_G * HD;
+      float* wml = a.ws_ml + (rk * a.max_chunks + cc.chunk) * 2 * MAX_G;
+#pragma unroll
+      for (int mt = 0; mt < KC; ++mt) {
+        const int d = mt * 16 + g8;
+        __stcg(&wo[h0 * HD + d], o[mt][0]);
+        __stcg(&wo[h1 * HD + d], o[mt][1]);
+        __stcg(&wo[h0 * HD + d + 8], o[mt][2]);
+        __stcg(&wo[h1 * HD + d + 8], o[mt][3]);
+      }
+      if (g8 == 0) {
+        __stcg(&wml[h0], mrun[0]);
+        __stcg(&wml[h1], mrun[1]);
+        __stcg(&wml[MAX_G + h0], l0);
+        __stcg(&wml[MAX_G + h1], l1);
+      }
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        // release: this warp's partial (written with st.cg, i.e. at L2) is
+        // visible before the count; the merging warp reads with ld.cg
+        int prev;
+        asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(prev) : "l"(&a.counters[rk]) : "memory");
+        last = prev == nchunks - 1;
+        if (last) a.counters[rk] = 0;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        // merge the chunks in order: lanes cover d, loop over the group's heads
+        const float* bo = a.ws_o + rk * a.max_chunks * MAX_G * HD;
+        const float* bml = a.ws_ml + rk * a.max_chunks * 2 * MAX_G;
+        for (int h = 0; h < G; ++h) {
+          float M = -INFINITY;
+          for (int c = 0; c < nchunks; ++c) M = fmaxf(M, __ldcg(&bml[c * 2 * MAX_G + h]));
+          float acc[HD / 32], l = 0.f;
+#pragma unroll
+          for (int e = 0; e < HD / 32; ++e) acc[e] = 0.f;
+          for (int c = 0; c < nchunks; ++c) {
+            const float f = exp2f(__ldcg(&bml[c * 2 * MAX_G + h]) - M);
+            l += __ldcg(&bml[c * 2 * MAX_G + MAX_G + h]) * f;
+#pragma unroll
+            for (int e = 0; e < HD / 32; ++e) acc[e] += __ldcg(&bo[(c * MAX_G + h) * HD + e * 32 + lane]) * f;
+          }
+          const float inv = 1.f / l;
+          bf16* dst = a.out + ((size_t)r * a.H + kvh * G + h) * HD;
+#pragma unroll
+          for (int e = 0; e < HD / 32; ++e) dst[e * 32 + lane] = __float2bfloat16(acc[e] * inv);
+        }
+      }
     }
-  }
-  if (single) return;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int* ctr = a.counters + (size_t)r * a.Hkv + kvh;
-    const int prev = atomicAdd(ctr, 1);
-    s_last = prev == nsplit - 1;
-    if (s_last) *ctr = 0;
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int e = threadIdx.x; e < G * HD; e += blockDim.x) {
-    const int h = e / HD, d = e % HD;
-    const int head = kvh * G + h;
-    const size_t base = ((size_t)r * a.H + head) * a.max_splits;
-    float M = -INFINITY;
-    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(&a.ws_ml[(base + s) * 2]));
-    float acc = 0.f, l = 0.f;
-    for (int s = 0; s < nsplit; ++s) {
-      const float f = exp2f(__ldcg(&a.ws_ml[(base + s) * 2]) - M);
-      acc += __ldcg(&a.ws_o[(base + s) * HD + d]) * f;
-      l += __ldcg(&a.ws_ml[(base + s) * 2 + 1]) * f;
-    }
-    a.out[((size_t)r * a.H + head) * HD + d] = __float2bfloat16(acc / l);
+    c_live = n_live;
+    cc = cn;
   }
 }
 
-template <int HD>
-int launch_attn(const CUtensorMap* tm, const AttnArgs& a, int M, cudaStream_t st) {
-  constexpr int SMEM = WARPS * STAGES * 2 * 16 * HD * 2 + WARPS * STAGES * 8 + 1024;
-  static_assert(WARPS * (8 * HD + 16) * 4 <= WARPS * STAGES * 2 * 16 * HD * 2, "merge area must fit");
+template <int HD, int WARPS, int STAGES>
+int launch_cfg(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
+  using C = AttnCfg<HD, WARPS, STAGES>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(paged_attn_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaError_t e = cudaFuncSetAttribute(paged_attn_kernel<HD, WARPS, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr = true;
   }
-  dim3 grid(M, a.Hkv, a.max_splits);
-  paged_attn_kernel<HD><<<grid, WARPS * 32, SMEM, st>>>(*tm, a);
-  return (int)cudaGetLastError();
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long long items = (long long)a.M * a.Hkv * a.max_chunks;
+  const int per_sm = (227 * 1024) / C::SMEM;
+  long long grid = (long long)sms * (per_sm > 0 ? per_sm : 1);
+  const long long need = (items + WARPS - 1) / WARPS;
+  if (grid > need) grid = need;
+  return (int)launch_k(paged_attn_kernel<HD, WARPS, STAGES>, dim3((int)grid), dim3(WARPS * 32), C::SMEM, st, *tm, a);
+}
+
+int g_attn_cfg = -1;  // 0: 6w x 4st, 1: 12w x 2st, 2: 8w x 3st, 3: 4w x 2st (x2 CTA/SM)
+
+template <int HD>
+int launch_attn(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
+  if (g_attn_cfg < 0) {
+    const char* e = getenv("PM_ATTN_CFG");
+    g_attn_cfg = e ? atoi(e) : 1;
+  }
+  switch (g_attn_cfg) {
+    case 0: return launch_cfg<HD, 6, 4>(tm, a, st);
+    case 2: return launch_cfg<HD, 8, 3>(tm, a, st);
+    case 3: return launch_cfg<HD, 4, 2>(tm, a, st);
+    default: return launch_cfg<HD, 12, 2>(tm, a, st);
+  }
 }
 
 }  // namespace
 
 // q [M][H][hd] bf16 (RoPE'd), pool via `tmap_kv` (2-D view [blocks*16][L_s*2*Hkv*hd],
 // box [16][64], 128B swizzle), block_table [M][max_blocks], seq_lens [M] (cached
-// positions incl. the current token), out [M][H][hd] bf16.
+// positions incl. the current token), out [M][H][hd] bf16.  ws_o/ws_ml hold
+// [M][Hkv][max_chunks][8][hd] / [..][2][8] fp32; counters [M][Hkv] start at 0.
 extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_table,
                                   const int* seq_lens, void* out, float* ws_o, float* ws_ml, int* counters,
                                   int M, int H, int Hkv, int hd, int layer, int L_s, int max_blocks,
-                                  int max_splits, void* stream) {
+                                  int max_chunks, int blocks_per_chunk, void* stream) {
+  (void)L_s;
   if (M == 0) return 0;
   const int G = H / Hkv;
-  if (H % Hkv || G > 8 || max_splits < 1) return (int)cudaErrorInvalidValue;
-  if (max_splits * BLOCKS_PER_SPLIT < max_blocks) return (int)cudaErrorInvalidValue;
+  if (H % Hkv || G > MAX_G || max_chunks < 1 || blocks_per_chunk < 1) return (int)cudaErrorInvalidValue;
+  if (max_chunks * blocks_per_chunk < max_blocks) return (int)cudaErrorInvalidValue;
   AttnArgs a{reinterpret_cast<const bf16*>(q), block_table, seq_lens, reinterpret_cast<bf16*>(out),
-             ws_o, ws_ml, counters, H, Hkv, G, layer, L_s, max_blocks, max_splits,
+             ws_o, ws_ml, counters, M, H, Hkv, G, layer, max_blocks, max_chunks, blocks_per_chunk,
              1.4426950408889634f / sqrtf((float)hd)};
   auto tm = reinterpret_cast<const CUtensorMap*>(tmap_kv);
   auto st = reinterpret_cast<cudaStream_t>(stream);
-  if (hd == 128) return launch_attn<128>(tm, a, M, st);
-  if (hd == 64) return launch_attn<64>(tm, a, M, st);
+  if (hd == 128) return launch_attn<128>(tm, a, st);
+  if (hd == 64) return launch_attn<64>(tm, a, st);
   return (int)cudaErrorInvalidValue;
 }
 
-extern "C" int pm_attn_blocks_per_split(void) { return BLOCKS_PER_SPLIT; }
+extern "C" int pm_attn_blocks_per_split(void) { return 16; }
 
 extern "C" int pm_prepare_attention(void) {
-  constexpr int S128 = WARPS * STAGES * 2 * 16 * 128 * 2 + WARPS * STAGES * 8 + 1024;
-  constexpr int S64 = WARPS * STAGES * 2 * 16 * 64 * 2 + WARPS * STAGES * 8 + 1024;
-  cudaError_t e = cudaFuncSetAttribute(paged_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, S128);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(paged_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, S64);
+  cudaError_t e = cudaSuccess;
+#define PM_SET(HD, W, S)                                                                            \
+  if (e == cudaSuccess)                                                                             \
+    e = cudaFuncSetAttribute(paged_attn_kernel<HD, W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             AttnCfg<HD, W, S>::SMEM);
+  PM_SET(128, 6, 4) PM_SET(128, 12, 2) PM_SET(128, 8, 3) PM_SET(128, 4, 2)
+  PM_SET(64, 6, 4) PM_SET(64, 12, 2) PM_SET(64, 8, 3) PM_SET(64, 4, 2)
+#undef PM_SET
   return (int)e;
 }

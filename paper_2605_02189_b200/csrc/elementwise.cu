@@ -15,6 +15,8 @@ namespace {
 
 __global__ void embed_kernel(const int* __restrict__ tok_table, const int* __restrict__ slots,
                              const bf16* __restrict__ table, float* __restrict__ resid, int d) {
+  pdl_trigger();
+  pdl_wait();
   const int m = blockIdx.x;
   const int id = tok_table[slots ? slots[m] : m];
   const uint4* src = reinterpret_cast<const uint4*>(table + (size_t)id * d);
@@ -29,6 +31,8 @@ __global__ void embed_kernel(const int* __restrict__ tok_table, const int* __res
 // one CTA per row; 256 threads; d % 8 == 0
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const bf16* __restrict__ w,
                                bf16* __restrict__ y, int d, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int m = blockIdx.x;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)m * d);
   float ss = 0.f;
@@ -70,6 +74,8 @@ __global__ void qkv_rope_append_kernel(const bf16* __restrict__ qkv, bf16* __res
                                        int M, int H, int Hkv, int layer, int L_s, int max_blocks,
                                        float eps) {
   constexpr int HD = 32 * E;
+  pdl_trigger();
+  pdl_wait();
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int heads = H + 2 * Hkv;
@@ -134,6 +140,8 @@ __global__ void qkv_rope_append_kernel(const bf16* __restrict__ qkv, bf16* __res
 __global__ void argmax_reduce_kernel(const float* __restrict__ val, const int* __restrict__ idx,
                                      int n_tiles, int m_cap, int* __restrict__ out_ids,
                                      int* __restrict__ tok_table, const int* __restrict__ slots) {
+  pdl_trigger();
+  pdl_wait();
   const int m = blockIdx.x;
   float bv = -INFINITY;
   int bi = 0x7fffffff;
@@ -166,16 +174,18 @@ extern "C" int pm_embed(const int* tok_table, const int* slots, const void* tabl
                         int d, void* stream) {
   if (d % 8) return (int)cudaErrorInvalidValue;
   if (M == 0) return 0;
-  embed_kernel<<<M, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      tok_table, slots, reinterpret_cast<const bf16*>(table), resid, d);
+  cudaError_t e = launch_k(embed_kernel, dim3(M), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), tok_table,
+                           slots, reinterpret_cast<const bf16*>(table), resid, d);
+  if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }
 
 extern "C" int pm_rmsnorm(const float* x, const void* w, void* y, int M, int d, float eps, void* stream) {
   if (d % 8) return (int)cudaErrorInvalidValue;
   if (M == 0) return 0;
-  rmsnorm_kernel<<<M, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      x, reinterpret_cast<const bf16*>(w), reinterpret_cast<bf16*>(y), d, eps);
+  cudaError_t e = launch_k(rmsnorm_kernel, dim3(M), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), x,
+                           reinterpret_cast<const bf16*>(w), reinterpret_cast<bf16*>(y), d, eps);
+  if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }
 
@@ -192,21 +202,24 @@ extern "C" int pm_qkv_rope_append(const void* qkv, void* q_out, void* pool, cons
   auto p = reinterpret_cast<bf16*>(pool);
   auto qn = reinterpret_cast<const bf16*>(qn_w);
   auto kn = reinterpret_cast<const bf16*>(kn_w);
+  cudaError_t e;
   if (hd == 128)
-    qkv_rope_append_kernel<4><<<blocks, threads, 0, st>>>(a, q, p, block_table, positions, rope, qn, kn, M, H,
-                                                          Hkv, layer, L_s, max_blocks, eps);
+    e = launch_k(qkv_rope_append_kernel<4>, dim3(blocks), dim3(threads), 0, st, a, q, p, block_table, positions,
+                 rope, qn, kn, M, H, Hkv, layer, L_s, max_blocks, eps);
   else if (hd == 64)
-    qkv_rope_append_kernel<2><<<blocks, threads, 0, st>>>(a, q, p, block_table, positions, rope, qn, kn, M, H,
-                                                          Hkv, layer, L_s, max_blocks, eps);
+    e = launch_k(qkv_rope_append_kernel<2>, dim3(blocks), dim3(threads), 0, st, a, q, p, block_table, positions,
+                 rope, qn, kn, M, H, Hkv, layer, L_s, max_blocks, eps);
   else
     return (int)cudaErrorInvalidValue;
+  if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }
 
 extern "C" int pm_argmax_reduce(const float* val, const int* idx, int n_tiles, int M, int m_cap, int* out_ids,
                                 int* tok_table, const int* slots, void* stream) {
   if (M == 0) return 0;
-  argmax_reduce_kernel<<<M, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(val, idx, n_tiles, m_cap,
-                                                                               out_ids, tok_table, slots);
+  cudaError_t e = launch_k(argmax_reduce_kernel, dim3(M), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), val,
+                           idx, n_tiles, m_cap, out_ids, tok_table, slots);
+  if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
 }

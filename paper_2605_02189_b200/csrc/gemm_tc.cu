@@ -113,31 +113,32 @@ PM_DEV bool get_seg(const GemmArgs& a, long long lo, long long hi, int i, Seg& s
 // Epilogue of one output feature `n` (a row of D^T) over token columns
 // c0..c0+15.  Rows held by one warp are 32 consecutive features, so the
 // SiLU(gate)*up partner of row n (interleaved gate/up rows) is lane ^ 1.
+template <int NC = 16>
 PM_DEV void row_epilogue(const GemmArgs& a, int n, int tok_base, int tok_end, int c0, const float* v, int lane) {
   const bool row_ok = n < a.n_out;
   switch (a.epilogue) {
     case EPI_STORE_BF16: {
       bf16* o = reinterpret_cast<bf16*>(a.out);
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
+      for (int j = 0; j < NC; ++j)
         if (c0 + j < tok_end && row_ok) o[(size_t)(tok_base + c0 + j) * a.ld_out + n] = __float2bfloat16(v[j]);
       break;
     }
     case EPI_RESID_ADD_F32: {
       float* o = reinterpret_cast<float*>(a.out);
-      float r[16];
+      float r[NC];
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
+      for (int j = 0; j < NC; ++j)
         r[j] = (c0 + j < tok_end && row_ok) ? o[(size_t)(tok_base + c0 + j) * a.ld_out + n] : 0.f;
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
+      for (int j = 0; j < NC; ++j)
         if (c0 + j < tok_end && row_ok) o[(size_t)(tok_base + c0 + j) * a.ld_out + n] = r[j] + v[j];
       break;
     }
     case EPI_SILU_MUL: {
       bf16* o = reinterpret_cast<bf16*>(a.out);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
+      for (int j = 0; j < NC; ++j) {
         const float up = __shfl_xor_sync(0xffffffffu, v[j], 1);
         if ((lane & 1) == 0 && c0 + j < tok_end && row_ok)
           o[(size_t)(tok_base + c0 + j) * a.ld_out + (n >> 1)] = __float2bfloat16(silu(v[j]) * up);
@@ -148,7 +149,7 @@ PM_DEV void row_epilogue(const GemmArgs& a, int n, int tok_base, int tok_end, in
       if (a.out) {
         float* o = reinterpret_cast<float*>(a.out);
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < NC; ++j)
           if (c0 + j < tok_end && row_ok) o[(size_t)(tok_base + c0 + j) * a.ld_out + n] = v[j];
       }
       break;
@@ -186,6 +187,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
   const long long lo = range_lo(blockIdx.x, a.total, gridDim.x);
   const long long hi = range_lo(blockIdx.x + 1, a.total, gridDim.x);
 
+  pdl_trigger();
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmap_x);
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -202,21 +204,40 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
     if (lane == 0) {
       // ---------------- producer: one 32 KB bulk weight chunk + one X tile per stage
       const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+      // Weights do not depend on the previous kernel: stream the first stages
+      // of weights before waiting on it (the activation tiles wait).
+      int pre = 0;
+      {
+        Seg sg;
+        int it = 0;
+        for (int i = 0; it < C::STAGES && get_seg(a, lo, hi, i, sg); ++i) {
+          const int wunit = sg.unit % a.n_units;
+          for (int kb = sg.kb0; kb < sg.kb1 && it < C::STAGES; ++kb, ++it) {
+            mbar_arrive_expect_tx(&full[it], C::STAGE);
+            bulk_load(sa + it * A_BYTES, a.w + ((size_t)wunit * a.kb + kb) * A_BYTES, A_BYTES, &full[it], pol_w);
+          }
+        }
+        pre = it;
+      }
+      pdl_wait();
       int it = 0;
       Seg sg;
       for (int i = 0; get_seg(a, lo, hi, i, sg); ++i) {
         const int wunit = sg.unit % a.n_units, ttile = sg.unit / a.n_units;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
-          if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
-          mbar_arrive_expect_tx(&full[s], C::STAGE);
-          bulk_load(sa + s * A_BYTES, a.w + ((size_t)wunit * a.kb + kb) * A_BYTES, A_BYTES, &full[s], pol_w);
+          if (it >= pre) {
+            if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+            mbar_arrive_expect_tx(&full[s], C::STAGE);
+            bulk_load(sa + s * A_BYTES, a.w + ((size_t)wunit * a.kb + kb) * A_BYTES, A_BYTES, &full[s], pol_w);
+          }
           tma_load_2d(sb + s * C::B_BYTES, &tmap_x, &full[s], kb * BK, ttile * BN, pol_x);
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
+    pdl_wait();
     if (lane == 0) {
       // ---------------- MMA issuer
       constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
@@ -247,6 +268,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
     __syncwarp();
   } else {
     // ---------------- epilogue warps 2..5: TMEM lane quarter q = warp % 4
+    pdl_wait();
     const int q = warp & 3;
     const int wq = warp - EPI_WARP0;
     Seg sg;
@@ -323,10 +345,15 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
 
 // Finishes the units the stream-K partition split across CTAs: sums the
 // per-segment fp32 partials in segment order (deterministic) and applies the
-// epilogue.  One CTA per (split unit, 16-column chunk); thread = output row.
+// epilogue.  One CTA per (split unit, RC-column chunk); thread = output row;
+// every segment's loads are in flight at once (segments <= MAX_SEGS).
+constexpr int RC = 4, MAX_SEGS = 16;
+
 template <int BN>
 __global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) {
-  const int unit = blockIdx.x, c0 = blockIdx.y * 16;
+  pdl_trigger();
+  pdl_wait();
+  const int unit = blockIdx.x, c0 = blockIdx.y * RC;
   const long long T = a.total, G = grid;
   const long long first = owner_of((long long)unit * a.kb, T, G);
   const long long last = owner_of((long long)(unit + 1) * a.kb - 1, T, G);
@@ -339,30 +366,44 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) 
   const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
   const int n = wunit * UNIT_ROWS + r;
   const float* part = a.ws + (size_t)unit * a.max_segs * BN * UNIT_ROWS + (size_t)c0 * UNIT_ROWS + r;
-  float v[16];
+  // rounds of MAX_SEGS segments; each round issues all its loads before the
+  // first add (volatile), sums stay in segment order
+  float v[RC];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = 0.f;
-#pragma unroll 2
-  for (int s = 0; s < nseg; ++s) {
-    float t[16];
+  for (int j = 0; j < RC; ++j) v[j] = 0.f;
+  for (int s0 = 0; s0 < nseg; s0 += MAX_SEGS) {
+    float t[MAX_SEGS][RC];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) t[j] = __ldcg(part + ((size_t)s * BN + j) * UNIT_ROWS);
+    for (int s = 0; s < MAX_SEGS; ++s)
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] += t[j];
+      for (int j = 0; j < RC; ++j) {
+        float x = 0.f;
+        if (s0 + s < nseg)
+          asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(x) : "l"(part + ((size_t)(s0 + s) * BN + j) * UNIT_ROWS));
+        t[s][j] = x;
+      }
+#pragma unroll
+    for (int s = 0; s < MAX_SEGS; ++s)
+#pragma unroll
+      for (int j = 0; j < RC; ++j) asm volatile("" : "+f"(t[s][j]));
+#pragma unroll
+    for (int j = 0; j < RC; ++j)
+#pragma unroll
+      for (int s = 0; s < MAX_SEGS; ++s) v[j] += t[s][j];
   }
-  row_epilogue(a, n, tok_base, tok_end, c0, v, lane);
+  row_epilogue<RC>(a, n, tok_base, tok_end, c0, v, lane);
   if (a.epilogue == EPI_LOGITS_ARGMAX) {
-    __shared__ float sv[8][16];
-    __shared__ int si[8][16];
+    __shared__ float sv[8][RC];
+    __shared__ int si[8][RC];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < RC; ++j) {
       float bv = n < a.n_out ? v[j] : -INFINITY;
       int bi = n;
       warp_argmax(bv, bi);
       if (lane == 0) { sv[warp][j] = bv; si[warp][j] = bi; }
     }
     __syncthreads();
-    if (r < 16 && c0 + r < tok_end) {
+    if (r < RC && c0 + r < tok_end) {
       float bv = sv[0][r];
       int bi = si[0][r];
       for (int w = 1; w < 8; ++w)
@@ -382,11 +423,9 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st) {
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  gemm_stream_kernel<BN><<<grid, NUM_THREADS, C::SMEM, st>>>(*tx, a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(gemm_stream_kernel<BN>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, *tx, a);
   if (e != cudaSuccess || a.max_segs <= 1 || (a.debug & 1)) return (int)e;
-  gemm_reduce_kernel<BN><<<dim3(a.n_units * a.tok_tiles, BN / 16), 256, 0, st>>>(a, grid);
-  return (int)cudaGetLastError();
+  return (int)launch_k(gemm_reduce_kernel<BN>, dim3(a.n_units * a.tok_tiles, BN / RC), dim3(256), 0, st, a, grid);
 }
 
 }  // namespace

@@ -201,17 +201,30 @@ def pool_tmap(pool: torch.Tensor, L_s: int, Hkv: int, hd: int) -> TensorMap:
     return TensorMap(pool, width, n_rows, width * 2, 64, 16)
 
 
-def attn_blocks_per_split() -> int:
+def attn_blocks_per_chunk() -> int:
+    """KV blocks per attention work item (fixed: results depend only on a
+    request's own length)."""
     return _C.lib().pm_attn_blocks_per_split()
 
 
-def paged_attention(tmap_kv, q, block_table, seq_lens, out, ws_o, ws_ml, counters, M, H, Hkv, hd, layer,
-                    L_s, max_splits, stream=None, kv_tokens=0):
+class AttnWorkspace:
+    """Chunk partials [M][Hkv][chunks][8][hd] + (m, l), merge counters."""
+
+    def __init__(self, m_cap, Hkv, hd, max_blocks, device):
+        self.bpc = attn_blocks_per_chunk()
+        self.max_chunks = max(1, -(-max_blocks // self.bpc))
+        self.o = torch.empty(m_cap * Hkv * self.max_chunks * 8 * hd, dtype=torch.float32, device=device)
+        self.ml = torch.empty(m_cap * Hkv * self.max_chunks * 16, dtype=torch.float32, device=device)
+        self.counters = torch.zeros(m_cap * Hkv, dtype=torch.int32, device=device)
+
+
+def paged_attention(tmap_kv, q, block_table, seq_lens, out, ws: AttnWorkspace, M, H, Hkv, hd, layer,
+                    L_s, stream=None, kv_tokens=0):
     """``kv_tokens`` (sum of seq_lens, host-known) only feeds the optional timer."""
     def go():
         _C.call("pm_paged_attention", tmap_kv.ptr, _ptr(q), _ptr(block_table), _ptr(seq_lens), _ptr(out),
-                _ptr(ws_o), _ptr(ws_ml), _ptr(counters), M, H, Hkv, hd, layer, L_s, block_table.shape[1],
-                max_splits, _stream(stream))
+                _ptr(ws.o), _ptr(ws.ml), _ptr(ws.counters), M, H, Hkv, hd, layer, L_s, block_table.shape[1],
+                ws.max_chunks, ws.bpc, _stream(stream))
     if TIMER is None:
         go()
     else:

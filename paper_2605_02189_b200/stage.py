@@ -90,13 +90,10 @@ class StageExecutor:
         _C.call("pm_prepare_gemm")
         _C.call("pm_prepare_attention")
         # workspaces
-        self.max_splits_attn = max(1, math.ceil(max_blocks / ops.attn_blocks_per_split()))
         lins = [x[k] for x in self.W for k in ("qkv", "o", "gu", "down")] + ([self.lm_head] if last else [])
         self.gws = ops.GemmWorkspace(m_cap, ops.GemmWorkspace.floats_needed(lins, m_cap),
                                      max(l.n_units for l in lins), self.lm_head.n_units if last else 1, device)
-        self.ws_o = torch.empty(m_cap * s.H * self.max_splits_attn * s.hd, dtype=f32, device=device)
-        self.ws_ml = torch.empty(m_cap * s.H * self.max_splits_attn * 2, dtype=f32, device=device)
-        self.attn_ctr = torch.zeros(m_cap * s.Hkv, dtype=i32, device=device)
+        self.aws = ops.AttnWorkspace(m_cap, s.Hkv, s.hd, max_blocks, device)
 
     # ------------------------------------------------------------------ views
     def pool_view(self):
@@ -124,9 +121,8 @@ class StageExecutor:
             w["qkv"](self.xn_maps, M, ops.EPI_STORE_BF16, self.qkv, s.qkv_out, self.gws, stream)
             ops.qkv_rope_append(self.qkv, self.q, self.pool, self.block_table, self.positions, self.rope,
                                 w["q_norm"], w["k_norm"], M, s.H, s.Hkv, s.hd, li, self.L_s, s.eps, stream)
-            ops.paged_attention(self.pool_map, self.q, self.block_table, self.seq_lens, self.attn, self.ws_o,
-                                self.ws_ml, self.attn_ctr, M, s.H, s.Hkv, s.hd, li, self.L_s,
-                                self.max_splits_attn, stream, kv_tokens=kv_tokens)
+            ops.paged_attention(self.pool_map, self.q, self.block_table, self.seq_lens, self.attn, self.aws,
+                                M, s.H, s.Hkv, s.hd, li, self.L_s, stream, kv_tokens=kv_tokens)
             w["o"](self.attn_maps, M, ops.EPI_RESID_ADD, self.resid, s.d, self.gws, stream)
             ops.rmsnorm(self.resid, w["mlp_norm"], self.xn, M, s.eps, stream)
             w["gu"](self.xn_maps, M, ops.EPI_SILU_MUL, self.act, s.ffn, self.gws, stream)

@@ -149,17 +149,13 @@ def test_rope_append_and_paged_attention(spec):
     bt = torch.from_numpy(tables).to(DEV)
     pos = torch.tensor(lens, dtype=torch.int32, device=DEV)
     ops.qkv_rope_append(qkv, q_out, pool, bt, pos, rope, qn, kn, M, H, Hkv, hd, layer, L_s, spec.eps)
-    bps = ops.attn_blocks_per_split()
-    max_splits = math.ceil(max_blocks / bps)
-    ws_o = torch.empty(M * H * max_splits * hd, device=DEV)
-    ws_ml = torch.empty(M * H * max_splits * 2, device=DEV)
-    ctr = torch.zeros(M * Hkv, dtype=torch.int32, device=DEV)
+    aws = ops.AttnWorkspace(M, Hkv, hd, max_blocks, DEV)
     out = torch.empty(M, H, hd, dtype=torch.bfloat16, device=DEV)
     seq = pos + 1
     tmap = ops.pool_tmap(pool, L_s, Hkv, hd)
-    ops.paged_attention(tmap, q_out, bt, seq, out, ws_o, ws_ml, ctr, M, H, Hkv, hd, layer, L_s, max_splits)
+    ops.paged_attention(tmap, q_out, bt, seq, out, aws, M, H, Hkv, hd, layer, L_s)
     torch.cuda.synchronize()
-    assert (ctr == 0).all()
+    assert (aws.counters == 0).all()
     tab = rope_table(spec, 2048)
     x = qkv.float().cpu().numpy()
     Pn = P.float().cpu().numpy()

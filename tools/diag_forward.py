@@ -48,8 +48,8 @@ for li, w in enumerate(ex.W):
                         w["k_norm"], M, s.H, s.Hkv, s.hd, li, ex.L_s, s.eps)
     q = R(ref.rope(qkv[:s.H * s.hd].reshape(s.H, s.hd), 0, tab))
     cmp(f"L{li} q", ex.q[0], q)
-    ops.paged_attention(ex.pool_map, ex.q, ex.block_table, ex.seq_lens, ex.attn, ex.ws_o, ex.ws_ml,
-                        ex.attn_ctr, M, s.H, s.Hkv, s.hd, li, ex.L_s, ex.max_splits_attn)
+    ops.paged_attention(ex.pool_map, ex.q, ex.block_table, ex.seq_lens, ex.attn, ex.aws,
+                        M, s.H, s.Hkv, s.hd, li, ex.L_s)
     k = R(ref.rope(qkv[s.H * s.hd:(s.H + s.Hkv) * s.hd].reshape(s.Hkv, s.hd), 0, tab))
     v = qkv[(s.H + s.Hkv) * s.hd:].reshape(s.Hkv, s.hd)
     o = R(ref.attend(q, k[None], v[None], s.H // s.Hkv))
