@@ -60,7 +60,10 @@ class DecodeEngine:
     def __init__(self, spec: ModelSpec, state: SchedulerState, cfg: ClusterConfig, params: EstimatorParams,
                  requests: dict, *, pp: int = 1, device="cuda", mode="dynamic", quota_tokens=0,
                  seed: int = 0, m_cap: int = None, timing=True, kv_init="random", prompts=None,
-                 record_logits=False, max_pos=None, trace: EventTrace = None, graphs: bool = True):
+                 record_logits=False, max_pos=None, trace: EventTrace = None, graphs: bool = True,
+                 local_stages=None):
+        """``local_stages``: which of the ``pp`` stages this process hosts
+        (default all; one rank per stage under torchrun, see pipeline.py)."""
         self.spec, self.cfg, self.params = spec, cfg, params
         self.requests = requests
         self.dev = torch.device(device)
@@ -83,7 +86,8 @@ class DecodeEngine:
         self.trash_slot = len(rids)
         self.graphs = graphs
         self.stages = []
-        for s in range(pp):
+        self.pp = pp
+        for s in (range(pp) if local_stages is None else local_stages):
             ex = StageExecutor(spec, stage_layers(spec, pp, s), first=(s == 0), last=(s == pp - 1),
                                m_cap=self.m_cap, pool_blocks=pool_blocks, max_blocks=self.max_blocks,
                                n_slots=len(rids) + 1, device=self.dev, seed=seed, max_pos=self.max_pos,
