@@ -34,6 +34,11 @@ int pm_tmap_encode_2d(void* tmap_out, const void* gaddr, unsigned long long inne
                       int swizzle128);
 int pm_host_alloc(unsigned long long bytes, void** out);
 int pm_host_free(void* p);
+/* device address of pm_host_alloc memory (it is mapped: kernels may read it over PCIe) */
+int pm_host_device_ptr(void* host, void** dev);
+/* per-step metadata upload: dst[i][0..n[i]) <- src[i] (int32; src = pm_host_device_ptr addresses), a
+ * kernel on `stream` instead of a copy-engine DMA so it never queues behind KV prefetch copies */
+int pm_meta_upload(int count, void* const* dst, const void* const* src, const int* n, void* stream);
 /* dst_base+dst_off[i] <- src_base+src_off[i], `bytes` each; contiguous runs merged */
 int pm_copy_pieces(void* dst_base, const void* src_base, const long long* dst_off, const long long* src_off,
                    int n, unsigned long long bytes, void* stream);
@@ -45,15 +50,26 @@ int pm_rmsnorm(const float* x, const void* w, void* y, int M, int d, float eps, 
 /* stream-K tcgen05 GEMM over a packed weight ([units][K/64][2][128][64], 128B-swizzled) */
 int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok, int bn,
             int grid, int epilogue, void* out, int ld_out, float* ws, int max_segs, float* amax_val,
-            int* amax_idx, int m_cap, void* stream);
+            int* amax_idx, int m_cap, int* counters, const void* prefetch, unsigned long long prefetch_bytes,
+            void* stream);
+/* counters: int[2 * n_units * ceil(m_tok/bn)], zero before the first call; every call leaves them zero.
+ * prefetch/prefetch_bytes: optional region the NEXT operation reads first; it is pulled into L2 while
+ * this GEMM drains (keeps HBM busy across the kernel boundary); NULL/0 for none. */
 int pm_gemm_max_segments(long long total, int kb, int grid);
 int pm_qkv_rope_append(const void* qkv, void* q_out, void* pool, const int* block_table, const int* positions,
                        const float* rope, const void* qn_w, const void* kn_w, int M, int H, int Hkv, int hd,
                        int layer, int L_s, int max_blocks, float eps, void* stream);
 int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_table, const int* seq_lens,
-                       void* out, float* ws_o, float* ws_ml, int* counters, int M, int H, int Hkv, int hd,
+                       const int* work, void* out, float* ws_o, float* ws_ml, int* counters, int M, int H,
+                       int Hkv, int hd,
                        int layer, int L_s, int max_blocks, int max_chunks, int blocks_per_chunk, void* stream);
 int pm_attn_blocks_per_split(void);
+/* host: a step's attention work list -- non-empty (chunk, row) pairs chunk-major, stably sorted by size
+ * descending, odd rounds of workers/hkv entries reversed; work[0] = count, entry j = {(chunk << 16) | row,
+ * seq_len} at work[2 + 2j]; work holds 2 + 2 * M * ceil(max_blocks / blocks_per_chunk) ints */
+int pm_attn_work_list(const int* seq_lens, int M, int blocks_per_chunk, int hkv, int workers, int* work);
+/* warps of a full attention launch on the current device (the `workers` above) */
+int pm_attn_workers(int hd);
 /* one-time kernel attributes; call once per device before CUDA-graph capture */
 int pm_prepare_gemm(void);
 int pm_prepare_attention(void);

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpmb200.so")
+LIB_PATH = os.environ.get("PM_B200_LIB") or os.path.join(_HERE, "libpmb200.so")  # override: A/B tooling only
 
 _P, _I, _F, _U64, _LL = C.c_void_p, C.c_int, C.c_float, C.c_ulonglong, C.c_longlong
 
@@ -21,14 +21,18 @@ _SIGS = {
     "pm_tmap_encode_2d": [_P, _P, _U64, _U64, _U64, C.c_uint, C.c_uint, _I],
     "pm_host_alloc": [_U64, C.POINTER(_P)],
     "pm_host_free": [_P],
+    "pm_host_device_ptr": [_P, C.POINTER(_P)],
+    "pm_meta_upload": [_I, _P, _P, _P, _P],
     "pm_copy_pieces": [_P, _P, _P, _P, _I, _U64, _P],
-    "pm_gemm": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _P, _I, _P],
+    "pm_gemm": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _P, _I, _P, _P, _U64, _P],
     "pm_gemm_max_segments": [_LL, _I, _I],
     "pm_embed": [_P, _P, _P, _P, _I, _I, _P],
     "pm_rmsnorm": [_P, _P, _P, _I, _I, _F, _P],
     "pm_qkv_rope_append": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P],
     "pm_argmax_reduce": [_P, _P, _I, _I, _I, _P, _P, _P, _P],
-    "pm_paged_attention": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P],
+    "pm_paged_attention": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P],
+    "pm_attn_work_list": [_P, _I, _I, _I, _I, _P],
+    "pm_attn_workers": [_I],
     "pm_attn_blocks_per_split": [],
     "pm_prepare_gemm": [],
     "pm_prepare_attention": [],

@@ -46,7 +46,55 @@ extern "C" int pm_tmap_encode_2d(void* tmap_out, const void* gaddr, unsigned lon
 // Pinned, portable host memory for the KV host replica (the paper's "CPU KV
 // pool").  The caller owns it and frees it with pm_host_free.
 extern "C" int pm_host_alloc(unsigned long long bytes, void** out) {
-  return (int)cudaHostAlloc(out, bytes, cudaHostAllocPortable);
+  return (int)cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+}
+// Device-side address of pinned host memory from pm_host_alloc (zero-copy reads).
+extern "C" int pm_host_device_ptr(void* host, void** dev) {
+  return (int)cudaHostGetDevicePointer(dev, host, 0);
+}
+
+namespace {
+constexpr int MAX_META_SEGS = 8;
+struct MetaSegs {
+  int* dst[MAX_META_SEGS];
+  const int* src[MAX_META_SEGS];   // device addresses of mapped pinned host memory
+  int n[MAX_META_SEGS];
+  int count;
+};
+// One CTA per segment streams it from pinned host memory over PCIe with
+// 16-byte loads (the step's block tables / positions / work list).  A kernel,
+// not cudaMemcpyAsync: the copy engines are busy with KV prefetch DMAs, and a
+// small metadata copy queued behind a 100+ MB prefetch would stall the
+// compute stream for milliseconds.
+__global__ void __launch_bounds__(512) meta_upload_kernel(MetaSegs m) {
+  pdl_trigger();
+  pdl_wait();
+  const int s = blockIdx.x;
+  if (s >= m.count) return;
+  const int n = m.n[s];
+  const int* src = m.src[s];
+  int* dst = m.dst[s];
+  const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  const int n4 = vec ? n / 4 : 0;
+  for (int i = threadIdx.x; i < n4; i += blockDim.x)
+    reinterpret_cast<int4*>(dst)[i] = __ldcv(reinterpret_cast<const int4*>(src) + i);  // no caching: host rewrites it
+  for (int i = n4 * 4 + threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldcv(src + i);
+}
+}  // namespace
+
+// dst[i][0..n[i]) <- src[i][0..n[i]) (int32), src = device addresses of mapped
+// pinned host memory (pm_host_device_ptr), on `stream` (<= 8 segments).
+extern "C" int pm_meta_upload(int count, void* const* dst, const void* const* src, const int* n, void* stream) {
+  if (count < 0 || count > MAX_META_SEGS) return (int)cudaErrorInvalidValue;
+  if (count == 0) return 0;
+  MetaSegs m{};
+  for (int i = 0; i < count; ++i) {
+    m.dst[i] = static_cast<int*>(dst[i]);
+    m.src[i] = static_cast<const int*>(src[i]);
+    m.n[i] = n[i];
+  }
+  m.count = count;
+  return (int)launch_k(meta_upload_kernel, dim3(count), dim3(512), 0, reinterpret_cast<cudaStream_t>(stream), m);
 }
 extern "C" int pm_host_free(void* p) { return (int)cudaFreeHost(p); }
 

@@ -2,7 +2,11 @@
 // per request).  HBM-bound: every KV byte of the active micro-batch is read
 // exactly once per layer, so the kernel is built to keep every SM streaming.
 //
-// Work item = (request row, kv head, chunk of `bpc` 16-token KV blocks).
+// Work item = (request row, kv head, chunk of `bpc` 16-token KV blocks).  The
+// host lists the non-empty (chunk, row) pairs chunk-major (all first chunks,
+// then all second chunks, ...) once per step; item i of the launch is list
+// entry i / Hkv, kv head i % Hkv.  Full-size chunks therefore come first and
+// the ragged tails last, so the static round-robin over warps is balanced.
 // Persistent grid; every WARP is an independent worker that walks its share
 // of the items with its own STAGES-deep TMA pipeline that runs straight
 // across item boundaries (no CTA-wide barriers on the hot path):
@@ -21,11 +25,15 @@
 // only on the request's own length, so results are batch-invariant.
 #include <stdlib.h>
 
+#include <algorithm>
+#include <vector>
+
 #include "common.cuh"
 
 namespace {
 
 constexpr int MAX_G = 8;
+constexpr int MAX_BPC = 16;   // KV blocks per work item (pm_attn_blocks_per_split)
 
 PM_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -60,44 +68,50 @@ struct AttnArgs {
   bf16* out;               // [M][H][HD]
   float* ws_o;             // [M][Hkv][max_chunks][8][HD]
   float* ws_ml;            // [M][Hkv][max_chunks][2][8]
-  int* counters;           // [M][Hkv] zero at rest
+  int* counters;           // [M][Hkv] merge counts, zero at rest
+  const int* work;         // [0] = #entries, [2 + 2j] = (chunk << 16) | row, [3 + 2j] = seq len; chunk-major
   int M, H, Hkv, G, layer, max_blocks, max_chunks, bpc;
   float scale_log2;        // log2(e)/sqrt(hd)
+  int debug;               // profiling only: bit0 skip the math (memory pipeline alone), bit2 trace
 };
+__device__ unsigned long long g_attn_trace[148 * 16 * 4];  // per warp: start, first data, end, blocks
+PM_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
-// cursor over a warp's (item, block) sequence: items gw, gw+W, gw+2W, ...
+// A warp's items are gw, gw + W, gw + 2W, ... (W = warps in the grid).  Their
+// descriptors and KV block ids are loaded into the warp's shared memory in
+// windows of up to ITEM_WIN items, all loads in flight at once and before
+// griddepcontrol.wait (the host wrote them), so the streaming loop never
+// waits on metadata.
+constexpr int ITEM_WIN = 32;
+constexpr int WIN_IDS = 256;   // block-id slots per warp window
+
 struct Cursor {
-  int item, blk, nblk, r, kvh, chunk, b0;  // b0 = first block of the chunk
+  int j, blk, nblk, r, kvh, chunk, b0, seq;  // j = item index in the window; b0 = first block
 };
 
-PM_DEV bool item_setup(const AttnArgs& a, int item, Cursor& c) {
-  const int per_row = a.Hkv * a.max_chunks;
-  if (item >= a.M * per_row) return false;
-  c.item = item;
-  c.r = item / per_row;
-  const int rem = item % per_row;
-  c.kvh = rem / a.max_chunks;
-  c.chunk = rem % a.max_chunks;
-  const int nblk_total = (a.seq_lens[c.r] + 15) >> 4;
-  c.b0 = c.chunk * a.bpc;
-  c.nblk = min(a.bpc, nblk_total - c.b0);
+PM_DEV bool item_setup(const AttnArgs& a, const int4* itm, int j, int nw, Cursor& c) {
+  if (j >= nw) return false;
+  const int4 m = itm[j];   // (row, first block, kv head, seq len)
+  c.j = j;
+  c.r = m.x;
+  c.b0 = m.y;
+  c.kvh = m.z;
+  c.seq = m.w;
+  c.chunk = m.y / a.bpc;
+  c.nblk = min(a.bpc, ((c.seq + 15) >> 4) - c.b0);
   c.blk = 0;
   return true;
-}
-// advance to the first non-empty item at or after `item` (stride W)
-PM_DEV bool next_item(const AttnArgs& a, int item, int W, Cursor& c) {
-  while (item_setup(a, item, c)) {
-    if (c.nblk > 0) return true;
-    item += W;
-  }
-  return false;
 }
 
 template <int HD, int WARPS, int STAGES>
 struct AttnCfg {
   static constexpr int TILE = 16 * HD * 2;          // one K or V tile
   static constexpr int STAGE = 2 * TILE;
-  static constexpr int SMEM = WARPS * STAGES * STAGE + WARPS * (STAGES * 8 + 2 * 64 * 4) + 1024;
+  static constexpr int SMEM = WARPS * STAGES * STAGE + WARPS * (STAGES * 8 + ITEM_WIN * 16 + WIN_IDS * 4) + 1024;
 };
 
 // Q^T fragments of an item's GQA group straight from global (prefetched one
@@ -124,54 +138,25 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* wbuf = smem + warp * STAGES * C::STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * C::STAGE) + warp * STAGES;
-  // physical block ids of the producer's current item, staged once per item (2 slots by parity)
-  int* bids = reinterpret_cast<int*>(smem + WARPS * STAGES * C::STAGE + WARPS * STAGES * 8) + warp * 2 * 64;
+  uint8_t* meta = smem + WARPS * STAGES * C::STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(meta) + warp * STAGES;
+  int4* itm = reinterpret_cast<int4*>(meta + WARPS * STAGES * 8) + warp * ITEM_WIN;
+  int* bid = reinterpret_cast<int*>(meta + WARPS * STAGES * 8 + WARPS * ITEM_WIN * 16) + warp * WIN_IDS;
   const int W = gridDim.x * WARPS;
   const int gw = blockIdx.x * WARPS + warp;
   const int G = a.G;
 
   pdl_trigger();
+  const int tr_slot = (blockIdx.x * WARPS + warp) * 4;
+  const bool tr = (a.debug & 4) && blockIdx.x * WARPS + warp < 148 * 16;
+  if (tr && lane == 0) g_attn_trace[tr_slot] = gtimer();
   if (lane == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
   }
   __syncwarp();
-  pdl_wait();  // q and the appended KV come from the previous kernel
-
-  // producer cursor (lane 0 issues STAGES blocks ahead of the consumer)
-  Cursor pc;
-  bool p_live = next_item(a, gw, W, pc);
-  int issued = 0, p_items = 0;
-  auto stage_ids = [&]() {  // lane 0: this item's block ids -> smem slot (p_items & 1)
-    int* dst = bids + (p_items & 1) * 64;
-    const int* src = a.block_table + (size_t)pc.r * a.max_blocks + pc.b0;
-    for (int k = 0; k < pc.nblk; ++k) dst[k] = src[k];
-  };
-  if (lane == 0 && p_live) stage_ids();
-  auto issue_one = [&]() {  // lane 0
-    const int s = issued % STAGES;
-    uint8_t* dst = wbuf + s * C::STAGE;
-    const int phys = bids[(p_items & 1) * 64 + pc.blk];
-    const int col_k = ((a.layer * 2 + 0) * a.Hkv + pc.kvh) * HD;
-    const int col_v = ((a.layer * 2 + 1) * a.Hkv + pc.kvh) * HD;
-    const uint64_t pol = policy_evict_first();
-    mbar_arrive_expect_tx(&bars[s], 2 * C::TILE);
-#pragma unroll
-    for (int hh = 0; hh < HALVES; ++hh) {
-      tma_load_2d(dst + hh * 2048, &tmap_kv, &bars[s], col_k + hh * 64, phys * 16, pol);
-      tma_load_2d(dst + C::TILE + hh * 2048, &tmap_kv, &bars[s], col_v + hh * 64, phys * 16, pol);
-    }
-    ++issued;
-    if (++pc.blk == pc.nblk) {
-      p_live = next_item(a, pc.item + W, W, pc);
-      ++p_items;
-      if (p_live) stage_ids();
-    }
-  };
-  if (lane == 0) {
-    for (int k = 0; k < STAGES && p_live; ++k) issue_one();
-  }
+  const int n_items = __ldg(&a.work[0]) * a.Hkv;   // host-written: readable before the wait
+  const int win = min(ITEM_WIN, WIN_IDS / a.bpc);
 
   const int g8 = lane >> 2, t = lane & 3;
   // per-lane ldmatrix offsets inside a (swizzled) K tile and V tile
@@ -187,19 +172,66 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
       voff[kc] = C::TILE + (dv >> 6) * 2048 + sw128(vtok, (dv & 63) >> 3);
     }
   }
-  Cursor cc, cn;
-  bool c_live = next_item(a, gw, W, cc), n_live = false;
-  int consumed = 0;
-  uint32_t qf[KC][2], qn[KC][2];
-  if (c_live) load_q<HD>(a, cc, lane, qn);
-  float o[KC][4];
-  float mrun[2], lrun[2];
+  int issued = 0, consumed = 0;
+  bool waited = false;
+  for (int j0 = 0;; j0 += win) {
+    const int first = gw + j0 * W;
+    if (first >= n_items) break;
+    const int nw = min(win, (n_items - first + W - 1) / W);
+    // ---- window metadata: descriptors, then every block id, all in flight
+    if (lane < nw) {
+      const int it = first + lane * W;
+      const int2 e = __ldg(reinterpret_cast<const int2*>(a.work) + 1 + it / a.Hkv);
+      itm[lane] = make_int4(e.x & 0xffff, (e.x >> 16) * a.bpc, it % a.Hkv, e.y);
+    }
+    __syncwarp();
+    for (int idx = lane; idx < nw * a.bpc; idx += 32) {
+      const int4 m = itm[idx / a.bpc];
+      const int k = idx % a.bpc;
+      const int nb = ((m.w + 15) >> 4) - m.y;
+      bid[idx] = k < nb ? __ldg(&a.block_table[(size_t)m.x * a.max_blocks + m.y + k]) : 0;
+    }
+    __syncwarp();
+    if (!waited) {
+      pdl_wait();  // q and the appended KV come from the previous kernel
+      waited = true;
+    }
+
+    // producer cursor (lane 0 issues STAGES blocks ahead of the consumer)
+    Cursor pc;
+    bool p_live = item_setup(a, itm, 0, nw, pc);
+    auto issue_one = [&]() {  // lane 0
+      const int s = issued % STAGES;
+      uint8_t* dst = wbuf + s * C::STAGE;
+      const int phys = bid[pc.j * a.bpc + pc.blk];
+      const int col_k = ((a.layer * 2 + 0) * a.Hkv + pc.kvh) * HD;
+      const int col_v = ((a.layer * 2 + 1) * a.Hkv + pc.kvh) * HD;
+      const uint64_t pol = policy_evict_first();
+      mbar_arrive_expect_tx(&bars[s], 2 * C::TILE);
+#pragma unroll
+      for (int hh = 0; hh < HALVES; ++hh) {
+        tma_load_2d(dst + hh * 2048, &tmap_kv, &bars[s], col_k + hh * 64, phys * 16, pol);
+        tma_load_2d(dst + C::TILE + hh * 2048, &tmap_kv, &bars[s], col_v + hh * 64, phys * 16, pol);
+      }
+      ++issued;
+      if (++pc.blk == pc.nblk) p_live = item_setup(a, itm, pc.j + 1, nw, pc);
+    };
+    if (lane == 0) {
+      for (int k = 0; k < STAGES && p_live; ++k) issue_one();
+    }
+
+    Cursor cc, cn;
+    bool c_live = item_setup(a, itm, 0, nw, cc), n_live = false;
+    uint32_t qf[KC][2], qn[KC][2];
+    if (c_live) load_q<HD>(a, cc, lane, qn);
+    float o[KC][4];
+    float mrun[2], lrun[2];
   while (c_live) {
     if (cc.blk == 0) {
       // new item: take the prefetched Q^T, prefetch the next item's, reset
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) { qf[kc][0] = qn[kc][0]; qf[kc][1] = qn[kc][1]; }
-      n_live = next_item(a, cc.item + W, W, cn);
+      n_live = item_setup(a, itm, cc.j + 1, nw, cn);
       if (n_live) load_q<HD>(a, cn, lane, qn);
 #pragma unroll
       for (int i = 0; i < KC; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
@@ -208,6 +240,16 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
     }
     const int s = consumed % STAGES;
     mbar_wait(&bars[s], (consumed / STAGES) & 1);
+    if (tr && consumed == 0 && lane == 0) g_attn_trace[tr_slot + 1] = gtimer();
+    if (a.debug & 1) {
+      __syncwarp();
+      ++consumed;
+      if (lane == 0 && p_live) issue_one();
+      if (++cc.blk < cc.nblk) continue;
+      c_live = n_live;
+      cc = cn;
+      continue;
+    }
     const uint32_t kbase = smem_u32(wbuf + s * C::STAGE);
     // ---- S^T = K Q^T
     float sc[4] = {0.f, 0.f, 0.f, 0.f}, sd[4] = {0.f, 0.f, 0.f, 0.f};  // two chains
@@ -222,7 +264,7 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
       for (int e = 0; e < 4; ++e) sc[e] += sd[e];
     }
     // ---- mask + online softmax (columns = heads 2t, 2t+1; rows = tokens g8, g8+8)
-    const int seq = a.seq_lens[cc.r];
+    const int seq = cc.seq;
     const int tok0 = (cc.b0 + cc.blk) * 16;
     const bool v0 = tok0 + g8 < seq, v1 = tok0 + g8 + 8 < seq;
     const float x0 = v0 ? sc[0] * a.scale_log2 : -INFINITY, x1 = v0 ? sc[1] * a.scale_log2 : -INFINITY;
@@ -255,10 +297,7 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
     }
     __syncwarp();
     ++consumed;
-    if (lane == 0 && p_live) {
-      fence_proxy_async();
-      issue_one();  // refill the slot just consumed
-    }
+    if (lane == 0 && p_live) issue_one();  // refill the slot just consumed (reads done: __syncwarp)
     if (++cc.blk < cc.nblk) continue;
 
     // ---- item done: per-column row sums, then store or stash the partial
@@ -317,32 +356,67 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
       }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
-        // merge the chunks in order: lanes cover d, loop over the group's heads
+        // merge the chunks in chunk order (online rescale, deterministic):
+        // lane covers 16 consecutive values of the group's flattened
+        // [head][dim] space per pass, 4 chunks' loads in flight per step
         const float* bo = a.ws_o + rk * a.max_chunks * MAX_G * HD;
         const float* bml = a.ws_ml + rk * a.max_chunks * 2 * MAX_G;
-        for (int h = 0; h < G; ++h) {
-          float M = -INFINITY;
-          for (int c = 0; c < nchunks; ++c) M = fmaxf(M, __ldcg(&bml[c * 2 * MAX_G + h]));
-          float acc[HD / 32], l = 0.f;
-#pragma unroll
-          for (int e = 0; e < HD / 32; ++e) acc[e] = 0.f;
-          for (int c = 0; c < nchunks; ++c) {
-            const float f = exp2f(__ldcg(&bml[c * 2 * MAX_G + h]) - M);
-            l += __ldcg(&bml[c * 2 * MAX_G + MAX_G + h]) * f;
-#pragma unroll
-            for (int e = 0; e < HD / 32; ++e) acc[e] += __ldcg(&bo[(c * MAX_G + h) * HD + e * 32 + lane]) * f;
+        for (int f0 = lane * 16; f0 < G * HD; f0 += 32 * 16) {
+          const int h = f0 / HD, d0 = f0 % HD;
+          float Mx = -INFINITY, Lx = 0.f, acc[16];
+      #pragma unroll
+          for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+          for (int c0 = 0; c0 < nchunks; c0 += 4) {
+            float m[4], l[4];
+            float4 ov[4][4];
+      #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const bool ok = c0 + j < nchunks;
+              m[j] = ok ? __ldcg(&bml[(c0 + j) * 2 * MAX_G + h]) : -INFINITY;
+              l[j] = ok ? __ldcg(&bml[(c0 + j) * 2 * MAX_G + MAX_G + h]) : 0.f;
+              const float4* src = reinterpret_cast<const float4*>(bo + ((c0 + j) * MAX_G + h) * HD + d0);
+      #pragma unroll
+              for (int v = 0; v < 4; ++v) ov[j][v] = ok ? __ldcg(src + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+      #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float Mn = fmaxf(Mx, m[j]);
+              const float s1 = Mx == -INFINITY ? 0.f : exp2f(Mx - Mn);
+              const float s2 = m[j] == -INFINITY ? 0.f : exp2f(m[j] - Mn);
+              Lx = Lx * s1 + l[j] * s2;
+      #pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                acc[4 * v + 0] = acc[4 * v + 0] * s1 + ov[j][v].x * s2;
+                acc[4 * v + 1] = acc[4 * v + 1] * s1 + ov[j][v].y * s2;
+                acc[4 * v + 2] = acc[4 * v + 2] * s1 + ov[j][v].z * s2;
+                acc[4 * v + 3] = acc[4 * v + 3] * s1 + ov[j][v].w * s2;
+              }
+              Mx = Mn;
+            }
           }
-          const float inv = 1.f / l;
-          bf16* dst = a.out + ((size_t)r * a.H + kvh * G + h) * HD;
-#pragma unroll
-          for (int e = 0; e < HD / 32; ++e) dst[e * 32 + lane] = __float2bfloat16(acc[e] * inv);
+          const float inv = 1.f / Lx;
+          uint32_t pk[8];
+      #pragma unroll
+          for (int e = 0; e < 8; ++e) pk[e] = pack_bf16(acc[2 * e] * inv, acc[2 * e + 1] * inv);
+          uint4* dst = reinterpret_cast<uint4*>(a.out + ((size_t)r * a.H + kvh * G + h) * HD + d0);
+          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
       }
     }
     c_live = n_live;
     cc = cn;
   }
+    __syncwarp();  // the window's smem metadata is reused by the next window
+  }
+  if (!waited) pdl_wait();
+  if (tr && lane == 0) {
+    g_attn_trace[tr_slot + 2] = gtimer();
+    g_attn_trace[tr_slot + 3] = consumed;
+  }
 }
+
+int num_sms();
 
 template <int HD, int WARPS, int STAGES>
 int launch_cfg(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
@@ -354,12 +428,7 @@ int launch_cfg(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return (int)e;
     attr = true;
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = num_sms();
   const long long items = (long long)a.M * a.Hkv * a.max_chunks;
   const int per_sm = (227 * 1024) / C::SMEM;
   long long grid = (long long)sms * (per_sm > 0 ? per_sm : 1);
@@ -370,13 +439,40 @@ int launch_cfg(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
 
 int g_attn_cfg = -1;  // 0: 6w x 4st, 1: 12w x 2st, 2: 8w x 3st, 3: 4w x 2st (x2 CTA/SM)
 
-template <int HD>
-int launch_attn(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
+int attn_cfg() {
   if (g_attn_cfg < 0) {
     const char* e = getenv("PM_ATTN_CFG");
     g_attn_cfg = e ? atoi(e) : 1;
   }
-  switch (g_attn_cfg) {
+  return g_attn_cfg;
+}
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+template <int HD, int WARPS, int STAGES>
+int workers_cfg() {
+  const int per_sm = (227 * 1024) / AttnCfg<HD, WARPS, STAGES>::SMEM;
+  return num_sms() * (per_sm > 0 ? per_sm : 1) * WARPS;
+}
+template <int HD>
+int attn_workers() {
+  switch (attn_cfg()) {
+    case 0: return workers_cfg<HD, 6, 4>();
+    case 2: return workers_cfg<HD, 8, 3>();
+    case 3: return workers_cfg<HD, 4, 2>();
+    default: return workers_cfg<HD, 12, 2>();
+  }
+}
+
+template <int HD>
+int launch_attn(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
+  switch (attn_cfg()) {
     case 0: return launch_cfg<HD, 6, 4>(tm, a, st);
     case 2: return launch_cfg<HD, 8, 3>(tm, a, st);
     case 3: return launch_cfg<HD, 4, 2>(tm, a, st);
@@ -388,20 +484,22 @@ int launch_attn(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
 
 // q [M][H][hd] bf16 (RoPE'd), pool via `tmap_kv` (2-D view [blocks*16][L_s*2*Hkv*hd],
 // box [16][64], 128B swizzle), block_table [M][max_blocks], seq_lens [M] (cached
-// positions incl. the current token), out [M][H][hd] bf16.  ws_o/ws_ml hold
-// [M][Hkv][max_chunks][8][hd] / [..][2][8] fp32; counters [M][Hkv] start at 0.
+// positions incl. the current token), work = the step's chunk-major (chunk, row)
+// list (see pm_attn_work_list), out [M][H][hd] bf16.  ws_o/ws_ml hold
+// [M][Hkv][max_chunks][8][hd] / [..][2][8] fp32 chunk partials; counters [M][Hkv]
+// start at 0 and are left at 0.
 extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_table,
-                                  const int* seq_lens, void* out, float* ws_o, float* ws_ml, int* counters,
-                                  int M, int H, int Hkv, int hd, int layer, int L_s, int max_blocks,
+                                  const int* seq_lens, const int* work, void* out, float* ws_o, float* ws_ml,
+                                  int* counters, int M, int H, int Hkv, int hd, int layer, int L_s, int max_blocks,
                                   int max_chunks, int blocks_per_chunk, void* stream) {
   (void)L_s;
   if (M == 0) return 0;
   const int G = H / Hkv;
   if (H % Hkv || G > MAX_G || max_chunks < 1 || blocks_per_chunk < 1) return (int)cudaErrorInvalidValue;
-  if (max_chunks * blocks_per_chunk < max_blocks) return (int)cudaErrorInvalidValue;
+  if (max_chunks * blocks_per_chunk < max_blocks || blocks_per_chunk > MAX_BPC) return (int)cudaErrorInvalidValue;
   AttnArgs a{reinterpret_cast<const bf16*>(q), block_table, seq_lens, reinterpret_cast<bf16*>(out),
-             ws_o, ws_ml, counters, M, H, Hkv, G, layer, max_blocks, max_chunks, blocks_per_chunk,
-             1.4426950408889634f / sqrtf((float)hd)};
+             ws_o, ws_ml, counters, work, M, H, Hkv, G, layer, max_blocks, max_chunks, blocks_per_chunk,
+             1.4426950408889634f / sqrtf((float)hd), getenv("PM_ATTN_DEBUG") ? atoi(getenv("PM_ATTN_DEBUG")) : 0};
   auto tm = reinterpret_cast<const CUtensorMap*>(tmap_kv);
   auto st = reinterpret_cast<cudaStream_t>(stream);
   if (hd == 128) return launch_attn<128>(tm, a, st);
@@ -409,7 +507,27 @@ extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int*
   return (int)cudaErrorInvalidValue;
 }
 
-extern "C" int pm_attn_blocks_per_split(void) { return 16; }
+extern "C" int pm_attn_blocks_per_split(void) {
+  static int bpc = 0;
+  if (!bpc) {
+    const char* e = getenv("PM_ATTN_BPC");  // tuning override
+    bpc = e ? atoi(e) : 12;
+    if (bpc < 1 || bpc > MAX_BPC) bpc = 12;
+  }
+  return bpc;
+}
+
+// Warps of a full attention launch (the `workers` of pm_attn_work_list).
+extern "C" int pm_attn_workers(int hd) {
+  if (hd == 128) return attn_workers<128>();
+  if (hd == 64) return attn_workers<64>();
+  return 0;
+}
+
+extern "C" int pm_attn_trace_read(void* dst) {
+  return (int)cudaMemcpyFromSymbol(dst, g_attn_trace, sizeof(g_attn_trace));
+}
+
 
 extern "C" int pm_prepare_attention(void) {
   cudaError_t e = cudaSuccess;
@@ -421,4 +539,49 @@ extern "C" int pm_prepare_attention(void) {
   PM_SET(64, 6, 4) PM_SET(64, 12, 2) PM_SET(64, 8, 3) PM_SET(64, 4, 2)
 #undef PM_SET
   return (int)e;
+}
+
+// Host helper: the work list of one step from its sequence lengths (what the
+// engine uploads with the block tables).  Entries are the non-empty (chunk,
+// row) pairs, chunk-major, then stably sorted by size (blocks) descending and
+// laid out "snake" over `workers` warps (odd rounds reversed) so every warp
+// gets a near-equal number of KV blocks.  Chunk boundaries still depend only
+// on each row's own length.  work holds 2 + 2 * M * ceil(max_blocks /
+// blocks_per_chunk) ints; work[0] = #entries, entry j at [2 + 2j] =
+// (chunk << 16) | row and [3 + 2j] = seq_lens[row].
+extern "C" int pm_attn_work_list(const int* seq_lens, int M, int blocks_per_chunk, int hkv, int workers,
+                                 int* work) {
+  if (M < 0 || M > 65535 || blocks_per_chunk < 1 || hkv < 1) return (int)cudaErrorInvalidValue;
+  int max_chunks = 0;
+  for (int r = 0; r < M; ++r) {
+    const int nc = (((seq_lens[r] + 15) >> 4) + blocks_per_chunk - 1) / blocks_per_chunk;
+    if (nc > max_chunks) max_chunks = nc;
+  }
+  std::vector<int> ent, size;
+  for (int c = 0; c < max_chunks; ++c)
+    for (int r = 0; r < M; ++r) {
+      const int nb = (seq_lens[r] + 15) >> 4;
+      const int sz = std::min(blocks_per_chunk, nb - c * blocks_per_chunk);
+      if (sz > 0) {
+        ent.push_back((c << 16) | r);
+        size.push_back(sz);
+      }
+    }
+  const int n = (int)ent.size();
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return size[x] > size[y]; });
+  if (workers > 0 && workers % hkv == 0) {
+    const int per_round = workers / hkv;
+    for (int j = 1; (j + 1) * per_round <= n; j += 2)
+      std::reverse(order.begin() + j * per_round, order.begin() + (j + 1) * per_round);
+  }
+  for (int i = 0; i < n; ++i) {
+    const int e = ent[order[i]];
+    work[2 + 2 * i] = e;
+    work[3 + 2 * i] = seq_lens[e & 0xffff];
+  }
+  work[0] = n;
+  work[1] = 0;
+  return 0;
 }

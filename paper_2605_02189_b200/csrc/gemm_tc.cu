@@ -14,8 +14,9 @@
 //     both 128-row halves of the unit (halves its SM ingress vs 128-row units);
 //   * persistent grid = #SMs, stream-K: the (unit, k-block) sequence is cut
 //     into #SMs equal contiguous ranges, so every SM streams the same bytes;
-//     a unit split between CTAs accumulates per-segment fp32 partials and the
-//     last CTA to finish it (atomic counter) sums them in segment order --
+//     a unit split between CTAs leaves per-segment fp32 partials in L2 and,
+//     at the end of the same kernel, each of its CTAs sums 1/nseg of the
+//     token columns in segment order (in-kernel fixup, no second launch) --
 //     boundaries depend only on (N, K, #SMs), never on M_tok, so every token's
 //     result is independent of its micro-batch mates (batch-invariant);
 //   * warp roles: w0 bulk/TMA producer, w1 MMA issuer (+TMEM owner), w2..w5
@@ -53,8 +54,12 @@ struct GemmArgs {
   float* amax_val;    // [units][m_cap]
   int* amax_idx;
   int m_cap;
+  int* counters;      // [units*tok_tiles][2] arrive / leave counts of split units, zero at rest
+  const uint8_t* pf;  // bytes the NEXT operation streams first: prefetched into L2 during this tail
+  unsigned long long pf_bytes;
   long long total;    // units * tok_tiles * kb
-  int debug;          // bit0: skip epilogue math (profiling only)
+  int fixup;          // 1: split units finished in-kernel (waits on co-resident CTAs); 0: gemm_reduce_kernel
+  int debug;          // profiling only: bit0 skip epilogue math, bit1 skip the fixup phase, bit2 skip partial stores
 };
 
 template <int BN>
@@ -157,6 +162,32 @@ PM_DEV void row_epilogue(const GemmArgs& a, int n, int tok_base, int tok_end, in
   }
 }
 
+// Epilogue of rows n and n+128 over 16 token columns; the residual-add reads
+// of both rows are issued before any store (one memory round trip).
+PM_DEV void pair_epilogue(const GemmArgs& a, int n, int tok_base, int tok_end, int c0, const float* v0,
+                          const float* v1, int lane) {
+  if (a.epilogue == EPI_RESID_ADD_F32) {
+    float* o = reinterpret_cast<float*>(a.out);
+    const bool ok0 = n < a.n_out, ok1 = n + 128 < a.n_out;
+    float r0[16], r1[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const size_t row = (size_t)(tok_base + c0 + j) * a.ld_out;
+      r0[j] = (c0 + j < tok_end && ok0) ? o[row + n] : 0.f;
+      r1[j] = (c0 + j < tok_end && ok1) ? o[row + n + 128] : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const size_t row = (size_t)(tok_base + c0 + j) * a.ld_out;
+      if (c0 + j < tok_end && ok0) o[row + n] = r0[j] + v0[j];
+      if (c0 + j < tok_end && ok1) o[row + n + 128] = r1[j] + v1[j];
+    }
+    return;
+  }
+  row_epilogue<16>(a, n, tok_base, tok_end, c0, v0, lane);
+  row_epilogue<16>(a, n + 128, tok_base, tok_end, c0, v1, lane);
+}
+
 // warp-level (max, lowest index) over the rows a lane holds; lane 0 gets the result
 PM_DEV void warp_argmax(float& bv, int& bi) {
 #pragma unroll
@@ -166,6 +197,19 @@ PM_DEV void warp_argmax(float& bv, int& bi) {
     if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
   }
 }
+
+// profiling trace (PM_GEMM_DEBUG bit3): per CTA globaltimer stamps
+__device__ unsigned long long g_gemm_trace[148 * 8];
+PM_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PM_TRACE(slot)                                                              \
+  do {                                                                              \
+    if ((a.debug & 8) && threadIdx.x == EPI_WARP0 * 32 && blockIdx.x < 148)        \
+      g_gemm_trace[blockIdx.x * 8 + (slot)] = gtimer();                             \
+  } while (0)
 
 template <int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -179,7 +223,8 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;      // [2]
   uint64_t* tempty = tfull + 2;             // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* fbar = tempty + 2;              // stream-K fixup bulk loads
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fbar + 1);
   float* red_val = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE + 512);   // [4][BN]
   int* red_idx = reinterpret_cast<int*>(red_val + 4 * BN);
 
@@ -188,10 +233,12 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
   const long long hi = range_lo(blockIdx.x + 1, a.total, gridDim.x);
 
   pdl_trigger();
+  PM_TRACE(0);
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmap_x);
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
+    mbar_init(fbar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -232,6 +279,18 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
             bulk_load(sa + s * A_BYTES, a.w + ((size_t)wunit * a.kb + kb) * A_BYTES, A_BYTES, &full[s], pol_w);
           }
           tma_load_2d(sb + s * C::B_BYTES, &tmap_x, &full[s], kb * BK, ttile * BN, pol_x);
+        }
+      }
+      // Every load of this CTA is issued: queue this CTA's share of the next
+      // operation's first bytes behind them, so HBM keeps streaming through
+      // this kernel's fixup/exit and the next kernel's ramp (it reads from L2).
+      if (a.pf_bytes) {
+        const unsigned long long share = ((a.pf_bytes / gridDim.x) + 15) & ~15ull;
+        const unsigned long long b0 = share * blockIdx.x;
+        const unsigned long long b1 = min(a.pf_bytes & ~15ull, b0 + share);
+        for (unsigned long long o = b0; o < b1; o += 65536) {
+          const uint32_t len = (uint32_t)min(65536ull, b1 - o);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf + o), "r"(len) : "memory");
         }
       }
     }
@@ -289,8 +348,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
             float v0[16], v1[16];
             tmem_ld16(trow + (b * 2 + 0) * BN + c0, v0);
             tmem_ld16(trow + (b * 2 + 1) * BN + c0, v1);
-            row_epilogue(a, n0, tok_base, tok_end, c0, v0, lane);
-            row_epilogue(a, n0 + 128, tok_base, tok_end, c0, v1, lane);
+            pair_epilogue(a, n0, tok_base, tok_end, c0, v0, v1, lane);
             if (argmax) {
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
@@ -303,9 +361,9 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
             }
           }
         } else {
-          // partial segment: fp32 [seg][col][256 rows]; gemm_reduce_kernel finishes the unit
+          // partial segment: fp32 [seg][col][256 rows] at L2; the fixup phase below finishes the unit
           float* dst = a.ws + ((size_t)sg.unit * a.max_segs + sg.seg) * (size_t)BN * UNIT_ROWS;
-          for (int c0 = 0; c0 < BN && c0 < tok_end; c0 += 16) {
+          for (int c0 = 0; c0 < BN && c0 < tok_end && !(a.debug & 4); c0 += 16) {
             float v0[16], v1[16];
             tmem_ld16(trow + (b * 2 + 0) * BN + c0, v0);
             tmem_ld16(trow + (b * 2 + 1) * BN + c0, v1);
@@ -321,6 +379,12 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
+      if (!whole && a.fixup && !(a.debug & 1)) {
+        // release this segment's partial: every writer fences, then one arrive
+        __threadfence();
+        epi_bar();
+        if (wq == 0 && lane == 0) atomicAdd(&a.counters[2 * sg.unit], 1);
+      }
       if (argmax && !(a.debug & 1)) {
         epi_bar();
         for (int c = threadIdx.x - EPI_WARP0 * 32; c < tok_end; c += 128) {
@@ -335,6 +399,111 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
           a.amax_idx[(size_t)wunit * a.m_cap + tok_base + c] = bi;
         }
         epi_bar();
+      }
+    }
+    // ---------------- stream-K fixup (in-kernel, all split units in parallel)
+    // Every CTA that holds a segment of a split unit finishes 1/nseg of its
+    // token columns: it waits until all nseg partials have arrived, sums them
+    // in segment order (deterministic; boundaries depend on N, K and #SMs
+    // only, so results stay batch-invariant) and applies the epilogue.  All
+    // CTAs are co-resident (grid <= #SMs, 1 CTA/SM) and every partial is
+    // written before any CTA waits, so the wait cannot deadlock.
+    PM_TRACE(1);
+    int ntr = 0;
+    if (a.fixup && !(a.debug & 3)) {
+      uint32_t fphase = 0;
+      for (int i = 0; get_seg(a, lo, hi, i, sg); ++i) {
+        if (sg.nseg == 1) continue;
+        const int tok_tile = sg.unit / a.n_units, wunit = sg.unit % a.n_units;
+        const int tok_base = tok_tile * BN;
+        const int tok_end = min(BN, a.m_tok - tok_base);
+        const int c_lo = sg.seg * tok_end / sg.nseg, c_hi = (sg.seg + 1) * tok_end / sg.nseg;
+        int* cnt = a.counters + 2 * sg.unit;
+        if (wq == 0 && lane == 0) {
+          int seen;
+          while (true) {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
+            if (seen >= sg.nseg) break;
+            __nanosleep(64);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        epi_bar();
+        if (ntr < 2) PM_TRACE(2 + 3 * ntr);
+        // the pipeline smem is idle now: stage every segment's column slice
+        // there with one bulk copy each ([seg][col][256 rows] is contiguous
+        // per segment), then sum from smem
+        const int r0 = q * 32 + lane;
+        const int n0 = wunit * UNIT_ROWS + r0;
+        const float* part = a.ws + (size_t)sg.unit * a.max_segs * BN * UNIT_ROWS;
+        const int chunk = max(1, (C::STAGES * C::STAGE) / (sg.nseg * UNIT_ROWS * 4));
+        const float* fb = reinterpret_cast<const float*>(smem);
+        for (int cc = c_lo; cc < c_hi; cc += chunk) {
+          const int nc = min(chunk, c_hi - cc);
+          if (wq == 0 && lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            mbar_arrive_expect_tx(fbar, (uint32_t)(sg.nseg * nc * UNIT_ROWS * 4));
+            for (int s2 = 0; s2 < sg.nseg; ++s2)
+              bulk_load(smem + (size_t)s2 * nc * UNIT_ROWS * 4, part + ((size_t)s2 * BN + cc) * UNIT_ROWS,
+                        (uint32_t)(nc * UNIT_ROWS * 4), fbar, pol);
+          }
+          mbar_wait(fbar, fphase);
+          fphase ^= 1;
+          if (ntr < 2 && cc == c_lo) PM_TRACE(3 + 3 * ntr);
+          // 16 columns per pass with every smem (and residual) load in flight
+          // before use: 4 warps per SM, so latency is hidden by ILP
+          for (int c = 0; c < nc; c += 16) {
+            float v0[16], v1[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v0[j] = v1[j] = 0.f;
+            for (int s2 = 0; s2 < sg.nseg; ++s2) {
+              const float* src = fb + ((size_t)s2 * nc + c) * UNIT_ROWS + r0;
+              float t0[16], t1[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                t0[j] = c + j < nc ? src[j * UNIT_ROWS] : 0.f;
+                t1[j] = c + j < nc ? src[j * UNIT_ROWS + 128] : 0.f;
+              }
+#pragma unroll
+              for (int j = 0; j < 16; ++j) { v0[j] += t0[j]; v1[j] += t1[j]; }
+            }
+            pair_epilogue(a, n0, tok_base, cc + nc, cc + c, v0, v1, lane);
+            if (a.epilogue == EPI_LOGITS_ARGMAX) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                float bv = n0 < a.n_out ? v0[j] : -INFINITY;
+                int bi = n0;
+                if (n0 + 128 < a.n_out && v1[j] > bv) { bv = v1[j]; bi = n0 + 128; }
+                warp_argmax(bv, bi);
+                if (lane == 0 && c + j < nc) { red_val[wq * BN + cc + c + j] = bv; red_idx[wq * BN + cc + c + j] = bi; }
+              }
+            }
+          }
+          // smem slice consumed before the next chunk's copies land
+          fence_proxy_async();
+          epi_bar();
+        }
+        if (a.epilogue == EPI_LOGITS_ARGMAX) {
+          for (int c = c_lo + threadIdx.x - EPI_WARP0 * 32; c < c_hi; c += 128) {
+            float bv = red_val[c];
+            int bi = red_idx[c];
+            for (int w = 1; w < 4; ++w)
+              if (red_val[w * BN + c] > bv || (red_val[w * BN + c] == bv && red_idx[w * BN + c] < bi)) {
+                bv = red_val[w * BN + c];
+                bi = red_idx[w * BN + c];
+              }
+            a.amax_val[(size_t)wunit * a.m_cap + tok_base + c] = bv;
+            a.amax_idx[(size_t)wunit * a.m_cap + tok_base + c] = bi;
+          }
+          epi_bar();
+        }
+        if (ntr < 2) PM_TRACE(4 + 3 * ntr);
+        ++ntr;
+        // the last CTA out of this unit re-arms its counters for the next launch
+        if (wq == 0 && lane == 0 && atomicAdd(cnt + 1, 1) == sg.nseg - 1) {
+          cnt[0] = 0;
+          cnt[1] = 0;
+        }
       }
     }
   }
@@ -424,11 +593,16 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st) {
     attr_set = true;
   }
   cudaError_t e = launch_k(gemm_stream_kernel<BN>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, *tx, a);
-  if (e != cudaSuccess || a.max_segs <= 1 || (a.debug & 1)) return (int)e;
+  if (e != cudaSuccess || a.fixup || a.max_segs <= 1 || (a.debug & 1)) return (int)e;
   return (int)launch_k(gemm_reduce_kernel<BN>, dim3(a.n_units * a.tok_tiles, BN / RC), dim3(256), 0, st, a, grid);
 }
 
 }  // namespace
+
+// Profiling only: copy the last traced launch's stamps ([148][8] u64 ns).
+extern "C" int pm_gemm_trace_read(void* dst) {
+  return (int)cudaMemcpyFromSymbol(dst, g_gemm_trace, sizeof(g_gemm_trace));
+}
 
 // One-time kernel attributes (call before any CUDA-graph capture).
 extern "C" int pm_prepare_gemm(void) {
@@ -458,12 +632,15 @@ extern "C" int pm_gemm_max_segments(long long total, int kb, int grid) {
 // swizzled K-major UMMA smem image (see ops.pack_weight).
 extern "C" int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
                        int bn, int grid, int epilogue, void* out, int ld_out, float* ws, int max_segs,
-                       float* amax_val, int* amax_idx, int m_cap, void* stream) {
+                       float* amax_val, int* amax_idx, int m_cap, int* counters, const void* prefetch,
+                       unsigned long long prefetch_bytes, void* stream) {
   if (k % BK || m_tok < 1 || m_tok > m_cap || grid < 1) return (int)cudaErrorInvalidValue;
   const int tok_tiles = (m_tok + bn - 1) / bn;
   GemmArgs a{reinterpret_cast<const uint8_t*>(w_packed), n_out, n_units, k / BK, m_tok, tok_tiles, epilogue,
-             out, ld_out, ws, max_segs, amax_val, amax_idx, m_cap,
-             (long long)n_units * tok_tiles * (k / BK), 0};
+             out, ld_out, ws, max_segs, amax_val, amax_idx, m_cap, counters,
+             reinterpret_cast<const uint8_t*>(prefetch), prefetch ? prefetch_bytes : 0ull,
+             (long long)n_units * tok_tiles * (k / BK), 0, 0};
+  if (getenv("PM_GEMM_FIXUP")) a.fixup = atoi(getenv("PM_GEMM_FIXUP"));
   if (getenv("PM_GEMM_DEBUG")) a.debug = atoi(getenv("PM_GEMM_DEBUG"));
   if (grid > a.total) grid = (int)a.total;
   auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);

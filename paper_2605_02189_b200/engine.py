@@ -29,6 +29,7 @@ import math
 import numpy as np
 import torch
 
+from . import _C, ops
 from .control import DecodeControl, StepWork
 from .kv import HostReplica, KvEngine
 from .model_core import ClusterConfig, EstimatorParams, blocks_for_tokens
@@ -39,11 +40,23 @@ from .trace import EpisodeMetrics, EventTrace
 
 
 class _MetaRing:
-    """Pinned host staging for per-step metadata; ``depth`` buffers so the
-    host can run ahead of the GPU without overwriting an in-flight copy."""
+    """Mapped pinned host staging for per-step metadata (pm_host_alloc);
+    ``depth`` buffers so the host can run ahead of the GPU without
+    overwriting one a meta_upload kernel has not read yet."""
 
-    def __init__(self, m_cap, max_blocks, depth=4):
-        self.bufs = [torch.zeros(m_cap * (max_blocks + 3), dtype=torch.int32).pin_memory() for _ in range(depth)]
+    def __init__(self, m_cap, max_blocks, depth=4, extra=0):
+        import ctypes
+        n = m_cap * (max_blocks + 3) + extra
+        self.bufs, self.dev_ptrs, self._raw = [], [], []
+        for _ in range(depth):
+            p = _C.C.c_void_p()
+            _C.call("pm_host_alloc", n * 4, _C.C.byref(p))
+            d = _C.C.c_void_p()
+            _C.call("pm_host_device_ptr", p, _C.C.byref(d))
+            arr = (ctypes.c_int32 * n).from_address(p.value)
+            self.bufs.append(torch.frombuffer(arr, dtype=torch.int32))
+            self.dev_ptrs.append(d.value)
+            self._raw.append(p.value)
         self.events = [None] * depth
         self.i = 0
         self.m_cap, self.max_blocks = m_cap, max_blocks
@@ -54,6 +67,13 @@ class _MetaRing:
         for ev in self.events[k] or ():
             ev.synchronize()
         return k, self.bufs[k]
+
+    def __del__(self):
+        try:
+            for p in self._raw:
+                _C.call("pm_host_free", _C.C.c_void_p(p))
+        except Exception:
+            pass
 
 
 class DecodeEngine:
@@ -96,7 +116,10 @@ class DecodeEngine:
                 ex.enable_logits()
             rep = HostReplica(len(rids), self.max_blocks, ex.block_bytes)
             self.stages.append((ex, KvEngine(ex, rep, self.slot_of, self.dev, timing=timing)))
-        self.meta = _MetaRing(self.m_cap, self.max_blocks)
+        self.work_len = self.stages[0][0].aws.work_len
+        self.bpc = self.stages[0][0].aws.bpc
+        self.attn_hkv, self.attn_workers = self.stages[0][0].aws.Hkv, self.stages[0][0].aws.workers
+        self.meta = _MetaRing(self.m_cap, self.max_blocks, extra=self.work_len)
         self.record_logits = record_logits
         self.logits_log = []   # (t, rows, positions, logits[M, V] np) when recording
         self.ids_log = []      # (t, rows, ids np)
@@ -215,14 +238,19 @@ class DecodeEngine:
         a[o + M + n:o + 2 * M] = 1
         a[o + 2 * M:o + 2 * M + n] = [self.slot_of[r] for r in rows]
         a[o + 2 * M + n:o + 3 * M] = self.trash_slot
+        # attention work list (chunk-major) over the bucket's rows, padding rows included
+        wo = o + 3 * M
+        ops.attn_work_list(a[o + M:o + 2 * M], self.bpc, self.attn_hkv, self.attn_workers, a[wo:wo + self.work_len])
+        wn = 2 + 2 * int(a[wo])
         evs = []
+        base = self.meta.dev_ptrs[k]
+        srcs = (_C.C.c_void_p * 5)(base, base + 4 * o, base + 4 * (o + M), base + 4 * (o + 2 * M), base + 4 * wo)
+        counts = (_C.C.c_int * 5)(M * mb, M, M, M, wn)
         for ex, kv in self.stages:
             s = kv.compute if stream is None else stream
-            with torch.cuda.stream(s):
-                ex.block_table[:M].view(-1).copy_(buf[:M * mb], non_blocking=True)
-                ex.positions[:M].copy_(buf[o:o + M], non_blocking=True)
-                ex.seq_lens[:M].copy_(buf[o + M:o + 2 * M], non_blocking=True)
-                ex.slots[:M].copy_(buf[o + 2 * M:o + 3 * M], non_blocking=True)
+            dsts = (_C.C.c_void_p * 5)(ex.block_table.data_ptr(), ex.positions.data_ptr(), ex.seq_lens.data_ptr(),
+                                       ex.slots.data_ptr(), ex.aws.work.data_ptr())
+            _C.call("pm_meta_upload", 5, dsts, srcs, counts, _C.C.c_void_p(s.cuda_stream))
             ev = torch.cuda.Event()
             ev.record(s)
             evs.append(ev)

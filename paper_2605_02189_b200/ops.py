@@ -128,6 +128,9 @@ class GemmWorkspace:
         self.ws = torch.empty(max(1, ws_floats), dtype=torch.float32, device=device)
         self.amax_val = torch.empty(max(1, vocab_units) * m_cap, dtype=torch.float32, device=device)
         self.amax_idx = torch.empty(max(1, vocab_units) * m_cap, dtype=torch.int32, device=device)
+        # stream-K fixup arrive/leave counters per (unit, token tile); kernels leave them zero
+        self.counters = torch.zeros(2 * max(1, max_units, vocab_units) * (-(-m_cap // 256)), dtype=torch.int32,
+                                    device=device)
 
     @staticmethod
     def floats_needed(linears, m_cap):
@@ -157,13 +160,17 @@ class Linear:
         return p
 
     def __call__(self, x_maps: dict, m_tok: int, epilogue: int, out, ld_out: int, ws: GemmWorkspace,
-                 stream=None):
+                 stream=None, prefetch=None):
+        """``prefetch``: optional (tensor, nbytes) the next operation reads
+        first; the kernel pulls it into L2 while it drains."""
         bn, grid, segs, tt = self.plan(m_tok)
+        pf_ptr, pf_bytes = (None, 0) if prefetch is None else (C.c_void_p(prefetch[0].data_ptr()), int(prefetch[1]))
 
         def go():
             _C.call("pm_gemm", _ptr(self.packed), x_maps[bn].ptr, self.n_out, self.n_units, self.k, m_tok, bn,
                     grid, epilogue, _ptr(out), ld_out, _ptr(ws.ws), segs,
-                    _ptr(ws.amax_val), _ptr(ws.amax_idx), ws.m_cap, _stream(stream))
+                    _ptr(ws.amax_val), _ptr(ws.amax_idx), ws.m_cap, _ptr(ws.counters), pf_ptr, pf_bytes,
+                    _stream(stream))
         if TIMER is None:
             go()
         else:
@@ -208,21 +215,69 @@ def attn_blocks_per_chunk() -> int:
 
 
 class AttnWorkspace:
-    """Chunk partials [M][Hkv][chunks][8][hd] + (m, l), merge counters."""
+    """Chunk partials [M][Hkv][chunks][8][hd] + (m, l), merge counters and the work list."""
 
     def __init__(self, m_cap, Hkv, hd, max_blocks, device):
         self.bpc = attn_blocks_per_chunk()
+        self.Hkv = Hkv
+        self.workers = attn_workers(hd) if torch.cuda.is_available() else 0
         self.max_chunks = max(1, -(-max_blocks // self.bpc))
         self.o = torch.empty(m_cap * Hkv * self.max_chunks * 8 * hd, dtype=torch.float32, device=device)
         self.ml = torch.empty(m_cap * Hkv * self.max_chunks * 16, dtype=torch.float32, device=device)
         self.counters = torch.zeros(m_cap * Hkv, dtype=torch.int32, device=device)
+        # the step's chunk-major work list (attn_work_list), uploaded with the metadata
+        self.work_len = 2 + 2 * m_cap * self.max_chunks
+        self.work = torch.zeros(self.work_len, dtype=torch.int32, device=device)
+
+    def set_work(self, seq_lens_host):
+        """Synchronous upload of the work list for ``seq_lens_host`` (tests /
+        smoke; the engine stages it through its pinned metadata ring)."""
+        w = attn_work_list(seq_lens_host, self.bpc, self.Hkv, self.workers)
+        self.work[:len(w)].copy_(torch.from_numpy(w))
+
+
+def attn_work_list(seq_lens, bpc: int, hkv: int = 1, workers: int = 0, out=None):
+    """The step's attention work list (mirrors pm_attn_work_list): the
+    non-empty (chunk, row) pairs chunk-major, stably sorted by size (blocks)
+    descending, odd rounds of ``workers // hkv`` entries reversed (snake), so
+    the kernel's round-robin gives every warp a near-equal number of KV
+    blocks.  Entry j is ``((chunk << 16) | row, seq_len)`` at
+    ``out[2 + 2j : 4 + 2j]``; ``out[0]`` = #entries."""
+    import numpy as np
+    seq = np.asarray(seq_lens, dtype=np.int64)
+    nb = (seq + 15) // 16
+    nc = (nb + bpc - 1) // bpc
+    cmax = int(nc.max()) if len(nc) else 0
+    mask = np.arange(cmax)[:, None] < nc[None, :]          # [chunk][row]
+    c_idx, r_idx = np.nonzero(mask)                           # chunk-major order
+    size = np.minimum(bpc, nb[r_idx] - c_idx * bpc)
+    order = np.argsort(-size, kind="stable")
+    n = len(order)
+    if workers > 0 and workers % hkv == 0:
+        per = workers // hkv
+        j = 1
+        while (j + 1) * per <= n:
+            order[j * per:(j + 1) * per] = order[j * per:(j + 1) * per][::-1]
+            j += 2
+    c_idx, r_idx = c_idx[order], r_idx[order]
+    if out is None:
+        out = np.zeros(2 + 2 * n, dtype=np.int32)
+    out[0], out[1] = n, 0
+    out[2:2 + 2 * n:2] = (c_idx << 16) | r_idx
+    out[3:3 + 2 * n:2] = seq[r_idx]
+    return out
+
+
+def attn_workers(hd: int) -> int:
+    """Warps of a full attention launch on this device (pm_attn_workers)."""
+    return _C.lib().pm_attn_workers(hd)
 
 
 def paged_attention(tmap_kv, q, block_table, seq_lens, out, ws: AttnWorkspace, M, H, Hkv, hd, layer,
                     L_s, stream=None, kv_tokens=0):
     """``kv_tokens`` (sum of seq_lens, host-known) only feeds the optional timer."""
     def go():
-        _C.call("pm_paged_attention", tmap_kv.ptr, _ptr(q), _ptr(block_table), _ptr(seq_lens), _ptr(out),
+        _C.call("pm_paged_attention", tmap_kv.ptr, _ptr(q), _ptr(block_table), _ptr(seq_lens), _ptr(ws.work), _ptr(out),
                 _ptr(ws.o), _ptr(ws.ml), _ptr(ws.counters), M, H, Hkv, hd, layer, L_s, block_table.shape[1],
                 ws.max_chunks, ws.bpc, _stream(stream))
     if TIMER is None:

@@ -27,6 +27,7 @@ def test_single_token_stage_forward(spec, pos):
     ex.block_table[0, :nb] = torch.tensor(table, dtype=torch.int32)
     ex.positions[0] = pos
     ex.seq_lens[0] = pos + 1
+    ex.aws.set_work([pos + 1])
     ex.slots[0] = 1
     ex.tok_table[1] = 4321 % s.vocab
     # random history KV for positions < pos (bf16) in every layer

@@ -50,6 +50,8 @@ def test_gemm_store_and_resid(n_out, k, m):
         lin(maps, 1, ops.EPI_STORE_BF16, y1, n_out, ws)
         torch.cuda.synchronize()
         assert torch.equal(y1[0], y[0])
+    # the in-kernel stream-K fixup re-arms its counters for the next launch
+    assert (ws.counters == 0).all()
 
 
 def test_gemm_silu_mul_interleaved():
@@ -153,6 +155,7 @@ def test_rope_append_and_paged_attention(spec):
     out = torch.empty(M, H, hd, dtype=torch.bfloat16, device=DEV)
     seq = pos + 1
     tmap = ops.pool_tmap(pool, L_s, Hkv, hd)
+    aws.set_work([L + 1 for L in lens])
     ops.paged_attention(tmap, q_out, bt, seq, out, aws, M, H, Hkv, hd, layer, L_s)
     torch.cuda.synchronize()
     assert (aws.counters == 0).all()
