@@ -80,20 +80,39 @@ def workload(spec_name="qwen3-8b", n_req=256, prompt=512, gen=512, m=2, cap_frac
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock and throttle reasons sampled every 20 ms by NVML while the
+    timed region runs (nvidia-smi one-shot queries as a fallback)."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
     def __init__(self, gpu=0):
         self.samples, self.stop = [], threading.Event()
         self.gpu = gpu
+        self.max_mhz = None
 
     def _run(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            while not self.stop.is_set():
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), int(get_r(h))))
+                self.stop.wait(0.02)
+            return
+        except Exception:
+            pass
+        q = "clocks.sm,clocks.max.sm"
         while not self.stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                self.samples.append([x.strip() for x in out.split(",")])
+                                     timeout=5).stdout.strip().split(",")
+                self.max_mhz = float(out[1])
+                self.samples.append((float(out[0]), 0))
             except Exception:
                 pass
             self.stop.wait(0.2)
@@ -101,6 +120,7 @@ class ClockSampler:
     def __enter__(self):
         self.th = threading.Thread(target=self._run, daemon=True)
         self.th.start()
+        time.sleep(0.1)
         return self
 
     def __exit__(self, *a):
@@ -108,17 +128,14 @@ class ClockSampler:
         self.th.join(timeout=10)
 
     def summary(self):
-        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        sm = sorted(x[0] for x in self.samples)
         reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for s in self.samples:
-            for i, n in enumerate(names):
-                if len(s) > 3 + i and "Active" in s[3 + i] and "Not" not in s[3 + i]:
-                    reasons.add(n)
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+        for _, r in self.samples:
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    reasons.add(name)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sm)}
 
 
 # ---------------------------------------------------------------- CPU leg
@@ -194,42 +211,55 @@ def run_ours(args):
     for _ in range(args.warmup):
         assert eng.step() is not None
     torch.cuda.synchronize()
-    ids_host = torch.zeros(args.steps, eng.m_cap, dtype=torch.int32).pin_memory()
+    ids_host = torch.zeros(2 * args.steps, eng.m_cap, dtype=torch.int32).pin_memory()
+    # ---- (1) device-timed region: K pipelined steps through the engine (the
+    # host control plane runs ahead of the GPU), CUDA events on the compute
+    # stream, barrier + synchronize on both sides, max over ranks
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    tokens = 0
-    meta_b = 0
-    h2d0, d2h0 = kv.h2d_bytes, kv.d2h_bytes
-    rec0 = len(kv.records)
+    tokens, h2d0, d2h0, rec0 = 0, kv.h2d_bytes, kv.d2h_bytes, len(kv.records)
+    kv_tok_sum = 0
     start_ev, end_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         start_ev.record(kv.compute)
-        w0 = time.perf_counter()
         for i in range(args.steps):
             work = eng.step()
             assert work is not None, "workload ended inside the timed region"
-            M = len(work.rows)
-            tokens += M
-            meta_b += eng.bucket(M) * (eng.max_blocks + 3) * 4
-            if ex.last:
-                with torch.cuda.stream(kv.compute):
-                    ids_host[i, :M].copy_(ex.out_ids[:M], non_blocking=True)
+            tokens += len(work.rows)
+            kv_tok_sum += sum(work.positions) + len(work.rows)
         end_ev.record(kv.compute)
         torch.cuda.synchronize()
-        wall = time.perf_counter() - w0
     dev_s = start_ev.elapsed_time(end_ev) * 1e-3
+    h2d_b, d2h_b = kv.h2d_bytes - h2d0, kv.d2h_bytes - d2h0
+    recs = kv.records[rec0:]
+    # ---- (2) end-to-end region: the same public call a serving loop makes,
+    # each step's greedy ids read back to pinned host memory and waited for
+    # before the next step starts (host<->device copies inside the region)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2e_tok, meta_b, e2e_h2d0, e2e_d2h0 = 0, 0, kv.h2d_bytes, kv.d2h_bytes
+    w0 = time.perf_counter()
+    for i in range(args.steps):
+        work = eng.step()
+        assert work is not None, "workload ended inside the e2e region"
+        M = len(work.rows)
+        e2e_tok += M
+        meta_b += (eng.bucket(M) * (eng.max_blocks + 3) + 2 + 2 * M * eng.stages[0][0].aws.max_chunks) * 4
+        last_ex, last_kv = eng.stages[-1]
+        with torch.cuda.stream(last_kv.compute):
+            ids_host[i, :M].copy_(last_ex.out_ids[:M], non_blocking=True)
+        last_kv.compute.synchronize()
+    wall = time.perf_counter() - w0
+    e2e_h2d, e2e_d2h = kv.h2d_bytes - e2e_h2d0, kv.d2h_bytes - e2e_d2h0
     if dist:
         t = torch.tensor([dev_s, wall], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_s, wall = t.tolist()
-        tokens_all = tokens  # every micro-batch row crosses all stages once
-    else:
-        tokens_all = tokens
-    h2d_b, d2h_b = kv.h2d_bytes - h2d0, kv.d2h_bytes - d2h0
-    # offload hiding over the timed steps
+    # offload hiding over the device-timed steps
     stall = h2d_busy = d2h_busy = 0.0
-    for r in kv.records[rec0:]:
+    for r in recs:
         if "ready" in r:
             stall += r["ready"].elapsed_time(r["start"]) * 1e-3
         if "h2d_start" in r:
@@ -238,8 +268,18 @@ def run_ours(args):
             d2h_busy += r["d2h_start"].elapsed_time(r["d2h_end"]) * 1e-3
     busy = h2d_busy + d2h_busy
     hidden = 1.0 - stall / busy if busy > 0 else 1.0
-    launches = args.steps * ex.kernels_per_step()
-    value = tokens_all / dev_s
+    M_avg = tokens / args.steps
+    launches = args.steps * (ex.kernels_per_step(eng.bucket(int(round(M_avg)))) + 1)  # + meta upload
+    value = tokens / dev_s
+    # decode roofline of the step: the slower of HBM bytes (weights
+    # + the micro-batch's KV + new KV + activations) and evicted-KV bytes over
+    # PCIe (measured H2D/D2H rates of this run)
+    hbm_bytes = sum(e.step_bytes(int(round(M_avg)), int(kv_tok_sum / args.steps - M_avg)) for e, _ in eng.stages)
+    t_hbm = hbm_bytes / (peaks["hbm_gbs"] * 1e9)
+    bw_h2d = h2d_b / h2d_busy if h2d_busy > 0 else None
+    bw_d2h = d2h_b / d2h_busy if d2h_busy > 0 else None
+    t_pcie = max((h2d_b / args.steps) / bw_h2d if bw_h2d else 0.0, (d2h_b / args.steps) / bw_d2h if bw_d2h else 0.0)
+    roof_tok_s = M_avg / max(t_hbm, t_pcie)
     out = {
         "metric": "offline decode tokens/sec (B200, KV offload on)",
         "value": value,
@@ -254,14 +294,21 @@ def run_ours(args):
         "dtype": "bf16",
         "data": "synthetic (random-init weights seeded N(0,0.02), random KV, random first tokens)",
         "config": desc,
-        "e2e": {"value": tokens_all / wall, "unit": "tokens/s",
-                "h2d_bytes_per_step": int((h2d_b + meta_b) / args.steps),
-                "d2h_bytes_per_step": int((d2h_b + tokens * 4) / args.steps),
-                "note": "public engine API (DecodeEngine.step, the simulate_decode loop): host control "
-                        "plane, metadata + KV prefetch H2D from pinned memory, KV offload + greedy ids D2H"},
+        "e2e": {"value": e2e_tok / wall, "unit": "tokens/s",
+                "h2d_bytes_per_step": int((e2e_h2d + meta_b) / args.steps),
+                "d2h_bytes_per_step": int((e2e_d2h + e2e_tok * 4) / args.steps),
+                "note": "K further steps through the public engine API (DecodeEngine.step, the simulate_decode "
+                        "loop), wall clock, each step's greedy ids copied to pinned host memory and waited for "
+                        "before the next step; H2D = KV prefetch + step metadata, D2H = KV offload + ids"},
         "kv_transfer_hidden_fraction": hidden,
         "kv_transfer": {"h2d_bytes": h2d_b, "d2h_bytes": d2h_b, "h2d_busy_s": h2d_busy,
-                        "d2h_busy_s": d2h_busy, "exposed_stall_s": stall},
+                        "d2h_busy_s": d2h_busy, "exposed_stall_s": stall,
+                        "h2d_GBps": bw_h2d / 1e9 if bw_h2d else None, "d2h_GBps": bw_d2h / 1e9 if bw_d2h else None},
+        "decode_roofline": {"hbm_bytes_per_step": hbm_bytes, "t_hbm_ms": t_hbm * 1e3, "t_pcie_ms": t_pcie * 1e3,
+                            "roofline_tok_s": roof_tok_s, "frac": value / roof_tok_s,
+                            "peak_hbm_gbs": peaks["hbm_gbs"], "peak_source": peaks_src,
+                            "note": "per step: weights once + the active micro-batch's KV + new KV + activations "
+                                    "over HBM vs prefetch/offload bytes over PCIe at this run's measured rates"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
@@ -336,7 +383,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=6)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-kernel-timing", dest="kernel_timing", action="store_false")

@@ -153,6 +153,11 @@ class Linear:
         self.weight_bytes = self.n_out * self.k * 2
         self._plans = {}
 
+    def launches(self, m_tok) -> int:
+        """Kernels one call launches: the stream-K GEMM, plus gemm_reduce when
+        the partition splits units."""
+        return 1 + (self.plan(m_tok)[2] > 1)
+
     def plan(self, m_tok):
         p = self._plans.get(m_tok)
         if p is None:

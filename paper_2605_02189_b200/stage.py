@@ -153,8 +153,16 @@ class StageExecutor:
         self.graphs[M] = g
         return g
 
-    def kernels_per_step(self) -> int:
-        return (1 if self.first else 0) + 8 * self.L_s + (3 if self.last else 0)
+    def kernels_per_step(self, M: int = None) -> int:
+        """Kernels of one forward(M): embed, per layer 2 rmsnorm + rope/append +
+        attention + 4 projections (each 1-2 launches), final norm + lm_head +
+        argmax."""
+        M = M or self.m_cap
+        n = (1 if self.first else 0) + 4 * self.L_s
+        n += sum(w[k].launches(M) for w in self.W for k in ("qkv", "o", "gu", "down"))
+        if self.last:
+            n += 2 + self.lm_head.launches(M)
+        return n
 
     # ------------------------------------------------------------------ roofline
     def step_bytes(self, M: int, kv_tokens: int) -> int:
