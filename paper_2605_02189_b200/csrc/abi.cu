@@ -67,8 +67,6 @@ struct MetaSegs {
 // small metadata copy queued behind a 100+ MB prefetch would stall the
 // compute stream for milliseconds.
 __global__ void __launch_bounds__(512) meta_upload_kernel(MetaSegs m) {
-  pdl_trigger();
-  pdl_wait();
   const int s = blockIdx.x;
   if (s >= m.count) return;
   const int n = m.n[s];
@@ -94,7 +92,14 @@ extern "C" int pm_meta_upload(int count, void* const* dst, const void* const* sr
     m.n[i] = n[i];
   }
   m.count = count;
-  return (int)launch_k(meta_upload_kernel, dim3(count), dim3(512), 0, reinterpret_cast<cudaStream_t>(stream), m);
+  // launched WITHOUT programmatic dependent launch: the step's kernels read
+  // this metadata before their griddepcontrol.wait (attention, fused QKV), so
+  // the dependent chain must start only after the upload has completed
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(count);
+  cfg.blockDim = dim3(512);
+  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+  return (int)cudaLaunchKernelEx(&cfg, meta_upload_kernel, m);
 }
 extern "C" int pm_host_free(void* p) { return (int)cudaFreeHost(p); }
 

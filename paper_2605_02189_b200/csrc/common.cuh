@@ -181,3 +181,6 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
+
+// internal launcher shared across translation units (elementwise.cu)
+int launch_rmsnorm(const float* x, const void* w, void* y, int M, int d, float eps, cudaStream_t st);

@@ -180,13 +180,17 @@ extern "C" int pm_embed(const int* tok_table, const int* slots, const void* tabl
   return (int)cudaGetLastError();
 }
 
-extern "C" int pm_rmsnorm(const float* x, const void* w, void* y, int M, int d, float eps, void* stream) {
+int launch_rmsnorm(const float* x, const void* w, void* y, int M, int d, float eps, cudaStream_t st) {
   if (d % 8) return (int)cudaErrorInvalidValue;
   if (M == 0) return 0;
-  cudaError_t e = launch_k(rmsnorm_kernel, dim3(M), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), x,
-                           reinterpret_cast<const bf16*>(w), reinterpret_cast<bf16*>(y), d, eps);
+  cudaError_t e = launch_k(rmsnorm_kernel, dim3(M), dim3(256), 0, st, x, reinterpret_cast<const bf16*>(w),
+                           reinterpret_cast<bf16*>(y), d, eps);
   if (e != cudaSuccess) return (int)e;
   return (int)cudaGetLastError();
+}
+
+extern "C" int pm_rmsnorm(const float* x, const void* w, void* y, int M, int d, float eps, void* stream) {
+  return launch_rmsnorm(x, w, y, M, d, eps, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int pm_qkv_rope_append(const void* qkv, void* q_out, void* pool, const int* block_table,

@@ -14,17 +14,20 @@
 //     both 128-row halves of the unit (halves its SM ingress vs 128-row units);
 //   * persistent grid = #SMs, stream-K: the (unit, k-block) sequence is cut
 //     into #SMs equal contiguous ranges, so every SM streams the same bytes;
-//     a unit split between CTAs leaves per-segment fp32 partials in L2 and,
-//     at the end of the same kernel, each of its CTAs sums 1/nseg of the
-//     token columns in segment order (in-kernel fixup, no second launch) --
-//     boundaries depend only on (N, K, #SMs), never on M_tok, so every token's
-//     result is independent of its micro-batch mates (batch-invariant);
+//     a unit split between CTAs leaves per-segment fp32 partials in L2 and a
+//     second kernel (launched with PDL) sums them in segment order and applies
+//     the epilogue -- fused with the consumer where one follows (residual add
+//     + the next RMSNorm; q/k-norm + RoPE + paged KV append).  Boundaries
+//     depend only on (N, K, #SMs), never on M_tok, so every token's result is
+//     independent of its micro-batch mates (batch-invariant);
 //   * warp roles: w0 bulk/TMA producer, w1 MMA issuer (+TMEM owner), w2..w5
 //     epilogue; the TMEM accumulator is double-buffered (BN <= 128) so the
 //     epilogue of one segment overlaps the mainloop of the next.
 // Epilogues: bf16 store, fp32 residual add, SiLU(gate)*up over interleaved
 // gate/up rows, fp32 logits + per-unit argmax partials.
 #include <stdlib.h>
+
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -54,12 +57,10 @@ struct GemmArgs {
   float* amax_val;    // [units][m_cap]
   int* amax_idx;
   int m_cap;
-  int* counters;      // [units*tok_tiles][2] arrive / leave counts of split units, zero at rest
   const uint8_t* pf;  // bytes the NEXT operation streams first: prefetched into L2 during this tail
   unsigned long long pf_bytes;
   long long total;    // units * tok_tiles * kb
-  int fixup;          // 1: split units finished in-kernel (waits on co-resident CTAs); 0: gemm_reduce_kernel
-  int debug;          // profiling only: bit0 skip epilogue math, bit1 skip the fixup phase, bit2 skip partial stores
+  int debug;          // profiling only: bit0 skip epilogue math, bit2 skip partial stores, bit3 trace
 };
 
 template <int BN>
@@ -223,8 +224,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;      // [2]
   uint64_t* tempty = tfull + 2;             // [2]
-  uint64_t* fbar = tempty + 2;              // stream-K fixup bulk loads
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fbar + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* red_val = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE + 512);   // [4][BN]
   int* red_idx = reinterpret_cast<int*>(red_val + 4 * BN);
 
@@ -238,7 +238,6 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
     tma_prefetch_desc(&tmap_x);
     for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
-    mbar_init(fbar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -283,7 +282,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
       }
       // Every load of this CTA is issued: queue this CTA's share of the next
       // operation's first bytes behind them, so HBM keeps streaming through
-      // this kernel's fixup/exit and the next kernel's ramp (it reads from L2).
+      // this kernel's drain/exit and the next kernel's ramp (it reads from L2).
       if (a.pf_bytes) {
         const unsigned long long share = ((a.pf_bytes / gridDim.x) + 15) & ~15ull;
         const unsigned long long b0 = share * blockIdx.x;
@@ -361,7 +360,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
             }
           }
         } else {
-          // partial segment: fp32 [seg][col][256 rows] at L2; the fixup phase below finishes the unit
+          // partial segment: fp32 [seg][col][256 rows] at L2; the post kernel finishes the unit
           float* dst = a.ws + ((size_t)sg.unit * a.max_segs + sg.seg) * (size_t)BN * UNIT_ROWS;
           for (int c0 = 0; c0 < BN && c0 < tok_end && !(a.debug & 4); c0 += 16) {
             float v0[16], v1[16];
@@ -379,12 +378,6 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
-      if (!whole && a.fixup && !(a.debug & 1)) {
-        // release this segment's partial: every writer fences, then one arrive
-        __threadfence();
-        epi_bar();
-        if (wq == 0 && lane == 0) atomicAdd(&a.counters[2 * sg.unit], 1);
-      }
       if (argmax && !(a.debug & 1)) {
         epi_bar();
         for (int c = threadIdx.x - EPI_WARP0 * 32; c < tok_end; c += 128) {
@@ -401,111 +394,6 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
         epi_bar();
       }
     }
-    // ---------------- stream-K fixup (in-kernel, all split units in parallel)
-    // Every CTA that holds a segment of a split unit finishes 1/nseg of its
-    // token columns: it waits until all nseg partials have arrived, sums them
-    // in segment order (deterministic; boundaries depend on N, K and #SMs
-    // only, so results stay batch-invariant) and applies the epilogue.  All
-    // CTAs are co-resident (grid <= #SMs, 1 CTA/SM) and every partial is
-    // written before any CTA waits, so the wait cannot deadlock.
-    PM_TRACE(1);
-    int ntr = 0;
-    if (a.fixup && !(a.debug & 3)) {
-      uint32_t fphase = 0;
-      for (int i = 0; get_seg(a, lo, hi, i, sg); ++i) {
-        if (sg.nseg == 1) continue;
-        const int tok_tile = sg.unit / a.n_units, wunit = sg.unit % a.n_units;
-        const int tok_base = tok_tile * BN;
-        const int tok_end = min(BN, a.m_tok - tok_base);
-        const int c_lo = sg.seg * tok_end / sg.nseg, c_hi = (sg.seg + 1) * tok_end / sg.nseg;
-        int* cnt = a.counters + 2 * sg.unit;
-        if (wq == 0 && lane == 0) {
-          int seen;
-          while (true) {
-            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
-            if (seen >= sg.nseg) break;
-            __nanosleep(64);
-          }
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-        }
-        epi_bar();
-        if (ntr < 2) PM_TRACE(2 + 3 * ntr);
-        // the pipeline smem is idle now: stage every segment's column slice
-        // there with one bulk copy each ([seg][col][256 rows] is contiguous
-        // per segment), then sum from smem
-        const int r0 = q * 32 + lane;
-        const int n0 = wunit * UNIT_ROWS + r0;
-        const float* part = a.ws + (size_t)sg.unit * a.max_segs * BN * UNIT_ROWS;
-        const int chunk = max(1, (C::STAGES * C::STAGE) / (sg.nseg * UNIT_ROWS * 4));
-        const float* fb = reinterpret_cast<const float*>(smem);
-        for (int cc = c_lo; cc < c_hi; cc += chunk) {
-          const int nc = min(chunk, c_hi - cc);
-          if (wq == 0 && lane == 0) {
-            const uint64_t pol = policy_evict_first();
-            mbar_arrive_expect_tx(fbar, (uint32_t)(sg.nseg * nc * UNIT_ROWS * 4));
-            for (int s2 = 0; s2 < sg.nseg; ++s2)
-              bulk_load(smem + (size_t)s2 * nc * UNIT_ROWS * 4, part + ((size_t)s2 * BN + cc) * UNIT_ROWS,
-                        (uint32_t)(nc * UNIT_ROWS * 4), fbar, pol);
-          }
-          mbar_wait(fbar, fphase);
-          fphase ^= 1;
-          if (ntr < 2 && cc == c_lo) PM_TRACE(3 + 3 * ntr);
-          // 16 columns per pass with every smem (and residual) load in flight
-          // before use: 4 warps per SM, so latency is hidden by ILP
-          for (int c = 0; c < nc; c += 16) {
-            float v0[16], v1[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v0[j] = v1[j] = 0.f;
-            for (int s2 = 0; s2 < sg.nseg; ++s2) {
-              const float* src = fb + ((size_t)s2 * nc + c) * UNIT_ROWS + r0;
-              float t0[16], t1[16];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                t0[j] = c + j < nc ? src[j * UNIT_ROWS] : 0.f;
-                t1[j] = c + j < nc ? src[j * UNIT_ROWS + 128] : 0.f;
-              }
-#pragma unroll
-              for (int j = 0; j < 16; ++j) { v0[j] += t0[j]; v1[j] += t1[j]; }
-            }
-            pair_epilogue(a, n0, tok_base, cc + nc, cc + c, v0, v1, lane);
-            if (a.epilogue == EPI_LOGITS_ARGMAX) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                float bv = n0 < a.n_out ? v0[j] : -INFINITY;
-                int bi = n0;
-                if (n0 + 128 < a.n_out && v1[j] > bv) { bv = v1[j]; bi = n0 + 128; }
-                warp_argmax(bv, bi);
-                if (lane == 0 && c + j < nc) { red_val[wq * BN + cc + c + j] = bv; red_idx[wq * BN + cc + c + j] = bi; }
-              }
-            }
-          }
-          // smem slice consumed before the next chunk's copies land
-          fence_proxy_async();
-          epi_bar();
-        }
-        if (a.epilogue == EPI_LOGITS_ARGMAX) {
-          for (int c = c_lo + threadIdx.x - EPI_WARP0 * 32; c < c_hi; c += 128) {
-            float bv = red_val[c];
-            int bi = red_idx[c];
-            for (int w = 1; w < 4; ++w)
-              if (red_val[w * BN + c] > bv || (red_val[w * BN + c] == bv && red_idx[w * BN + c] < bi)) {
-                bv = red_val[w * BN + c];
-                bi = red_idx[w * BN + c];
-              }
-            a.amax_val[(size_t)wunit * a.m_cap + tok_base + c] = bv;
-            a.amax_idx[(size_t)wunit * a.m_cap + tok_base + c] = bi;
-          }
-          epi_bar();
-        }
-        if (ntr < 2) PM_TRACE(4 + 3 * ntr);
-        ++ntr;
-        // the last CTA out of this unit re-arms its counters for the next launch
-        if (wq == 0 && lane == 0 && atomicAdd(cnt + 1, 1) == sg.nseg - 1) {
-          cnt[0] = 0;
-          cnt[1] = 0;
-        }
-      }
-    }
   }
   tc_fence_before();
   __syncthreads();
@@ -516,28 +404,25 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
 // per-segment fp32 partials in segment order (deterministic) and applies the
 // epilogue.  One CTA per (split unit, RC-column chunk); thread = output row;
 // every segment's loads are in flight at once (segments <= MAX_SEGS).
-constexpr int RC = 4, MAX_SEGS = 16;
+#ifndef PM_RC
+#define PM_RC 4
+#endif
+constexpr int RC = PM_RC, MAX_SEGS = 8;
 
-template <int BN>
-__global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) {
-  pdl_trigger();
-  pdl_wait();
-  const int unit = blockIdx.x, c0 = blockIdx.y * RC;
+// segment count of stream-K unit `unit` (mirrors get_seg / pm_gemm_max_segments)
+PM_DEV int unit_segments(const GemmArgs& a, int unit, int grid) {
   const long long T = a.total, G = grid;
   const long long first = owner_of((long long)unit * a.kb, T, G);
   const long long last = owner_of((long long)(unit + 1) * a.kb - 1, T, G);
-  const int nseg = (int)(last - first + 1);
-  if (nseg == 1) return;
-  const int tok_tile = unit / a.n_units, wunit = unit % a.n_units;
-  const int tok_base = tok_tile * BN;
-  const int tok_end = min(BN, a.m_tok - tok_base);
-  if (c0 >= tok_end) return;
-  const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
-  const int n = wunit * UNIT_ROWS + r;
+  return (int)(last - first + 1);
+}
+
+// v[j] = sum over the unit's segments (in segment order) of row r, column c0+j.
+// Rounds of MAX_SEGS segments; each round issues all its loads before the
+// first add (volatile keeps them in flight).
+template <int BN>
+PM_DEV void sum_partials(const GemmArgs& a, int unit, int nseg, int c0, int r, float (&v)[RC]) {
   const float* part = a.ws + (size_t)unit * a.max_segs * BN * UNIT_ROWS + (size_t)c0 * UNIT_ROWS + r;
-  // rounds of MAX_SEGS segments; each round issues all its loads before the
-  // first add (volatile), sums stay in segment order
-  float v[RC];
 #pragma unroll
   for (int j = 0; j < RC; ++j) v[j] = 0.f;
   for (int s0 = 0; s0 < nseg; s0 += MAX_SEGS) {
@@ -560,6 +445,25 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) 
 #pragma unroll
       for (int s = 0; s < MAX_SEGS; ++s) v[j] += t[s][j];
   }
+}
+
+// Finishes the units the stream-K partition split across CTAs and applies
+// the epilogue.  One CTA per (split unit, RC-column chunk); thread = row.
+template <int BN>
+__global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) {
+  pdl_trigger();
+  pdl_wait();
+  const int unit = blockIdx.x, c0 = blockIdx.y * RC;
+  const int nseg = unit_segments(a, unit, grid);
+  if (nseg == 1) return;
+  const int tok_tile = unit / a.n_units, wunit = unit % a.n_units;
+  const int tok_base = tok_tile * BN;
+  const int tok_end = min(BN, a.m_tok - tok_base);
+  if (c0 >= tok_end) return;
+  const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
+  const int n = wunit * UNIT_ROWS + r;
+  float v[RC];
+  sum_partials<BN>(a, unit, nseg, c0, r, v);
   row_epilogue<RC>(a, n, tok_base, tok_end, c0, v, lane);
   if (a.epilogue == EPI_LOGITS_ARGMAX) {
     __shared__ float sv[8][RC];
@@ -583,8 +487,216 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) 
   }
 }
 
+// ---------------------------------------------------------------- fused post kernels
+// (1) residual GEMM (O / down projection) -> resid += x W^T, then the NEXT
+// RMSNorm of every finished row: the CTA that completes a token row last
+// (per-row arrival count over the split units) normalises it into `xn`.
+// No CTA ever waits, so there is no co-residency assumption.
+struct NormArgs {
+  const bf16* w;      // [d] RMSNorm weight
+  bf16* xn;           // [m_cap][d] normalised output (the next GEMM's TMA source)
+  int* row_cnt;       // [m_cap] arrival counts, zero at rest
+  int n_split;        // units of this launch with > 1 segment (all arrive once per row)
+  float eps;
+};
+
+// RMSNorm of rows x[rows[j]] (fp32, row stride ld) -> y (bf16, row stride
+// d) by the whole CTA (256 threads), one row at a time held in registers:
+// one pass over L2 per row (d <= 256 * 4 * NORM_V4).  Same reduction tree as
+// rmsnorm_kernel, so the result is bit-identical to the unfused norm.
+constexpr int NORM_V4 = 8;   // d <= 8192
+PM_DEV void block_rmsnorm_rows(const float* x, int ld, const int* rows, int nrows, const bf16* w, bf16* y, int d,
+                               float eps) {
+  __shared__ float red[8];
+#pragma unroll 1
+  for (int j = 0; j < nrows; ++j) {
+    float4 v[NORM_V4];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < NORM_V4; ++i) {
+      const int c = threadIdx.x + i * 256;
+      v[i] = c < d / 4 ? __ldcg(reinterpret_cast<const float4*>(x + (size_t)rows[j] * ld) + c)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < NORM_V4; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    float t = (threadIdx.x & 31) < 8 ? red[threadIdx.x & 31] : 0.f;
+    t = __shfl_sync(0xffffffffu, warp_sum(t), 0);
+    const float r = rsqrtf(t / (float)d + eps);
+#pragma unroll
+    for (int i = 0; i < NORM_V4; ++i) {
+      const int c = threadIdx.x + i * 256;
+      if (c < d / 4) {
+        const uint2 ww = reinterpret_cast<const uint2*>(w)[c];
+        uint2 o;
+        o.x = pack_bf16(v[i].x * r * bf16_lo(ww.x), v[i].y * r * bf16_hi(ww.x));
+        o.y = pack_bf16(v[i].z * r * bf16_lo(ww.y), v[i].w * r * bf16_hi(ww.y));
+        reinterpret_cast<uint2*>(y + (size_t)rows[j] * d)[c] = o;
+      }
+    }
+    __syncthreads();  // red[] reused by the next row
+  }
+}
+
 template <int BN>
-int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st) {
+__global__ void __launch_bounds__(256) gemm_resid_norm_kernel(GemmArgs a, int grid, NormArgs na) {
+  pdl_trigger();
+  pdl_wait();
+  const int unit = blockIdx.x, c0 = blockIdx.y * RC;
+  const int nseg = unit_segments(a, unit, grid);
+  if (nseg == 1) return;  // whole units were added by the GEMM epilogue and do not count
+  const int tok_tile = unit / a.n_units, wunit = unit % a.n_units;
+  const int tok_base = tok_tile * BN;
+  const int tok_end = min(BN, a.m_tok - tok_base);
+  if (c0 >= tok_end) return;
+  const int r = threadIdx.x;
+  const int n = wunit * UNIT_ROWS + r;
+  float v[RC];
+  sum_partials<BN>(a, unit, nseg, c0, r, v);
+  float* o = reinterpret_cast<float*>(a.out);
+  if (n < a.n_out) {
+    float res[RC];   // every residual load in flight before the first store
+#pragma unroll
+    for (int j = 0; j < RC; ++j) res[j] = c0 + j < tok_end ? __ldcg(o + (size_t)(tok_base + c0 + j) * a.ld_out + n) : 0.f;
+#pragma unroll
+    for (int j = 0; j < RC; ++j)
+      if (c0 + j < tok_end) __stcg(o + (size_t)(tok_base + c0 + j) * a.ld_out + n, res[j] + v[j]);
+  }
+  // arrive on each finished row (the CTA's stores are ordered before the
+  // release by the barrier); the last unit to arrive normalises the row
+  __shared__ int last_rows[RC];
+  __shared__ int n_last;
+  if (r == 0) n_last = 0;
+  __syncthreads();
+  if (r < RC && c0 + r < tok_end) {
+    int prev;
+    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(prev) : "l"(na.row_cnt + tok_base + c0 + r) : "memory");
+    if (prev == na.n_split - 1) {
+      na.row_cnt[tok_base + c0 + r] = 0;
+      last_rows[atomicAdd(&n_last, 1)] = tok_base + c0 + r;
+    }
+  }
+  __syncthreads();
+  if (n_last) block_rmsnorm_rows(o, a.ld_out, last_rows, n_last, na.w, na.xn, a.n_out, na.eps);
+}
+
+// (2) fused QKV projection -> (Qwen3 q/k RMSNorm) + RoPE + paged KV append.
+// One CTA per (unit = 256 output features = 256/hd whole heads, RC tokens);
+// thread = feature.  Split units are summed from the partials, whole units
+// read the bf16 the GEMM epilogue stored; either way the value is rounded to
+// bf16 first (the same rounding the unfused qkv buffer applies).
+struct RopeArgs {
+  bf16* q_out;              // [M][H][hd]
+  bf16* pool;               // block-first KV pool
+  const int* block_table;   // [M][max_blocks]
+  const int* positions;     // [M]
+  const float* rope;        // [pos][hd] cos | sin
+  const bf16* qn_w;         // [hd] or null
+  const bf16* kn_w;
+  int H, Hkv, hd, layer, L_s, max_blocks;
+  float eps;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(256) gemm_qkv_rope_kernel(GemmArgs a, int grid, RopeArgs ra) {
+  pdl_trigger();
+  const int unit = blockIdx.x, c0 = blockIdx.y * RC;
+  const int tok_tile = unit / a.n_units, wunit = unit % a.n_units;
+  const int tok_base = tok_tile * BN;
+  const int tok_end = min(BN, a.m_tok - tok_base);
+  if (c0 >= tok_end) return;
+  const int nseg = unit_segments(a, unit, grid);
+  const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
+  const int n = wunit * UNIT_ROWS + r;
+  const bool row_ok = n < a.n_out;
+  const int hd = ra.hd, hg = n / hd, d = n % hd, half = hd / 2;   // global head, dim
+  const bool is_q = hg < ra.H, is_k = !is_q && hg < ra.H + ra.Hkv;
+  const bf16* nw = is_q ? ra.qn_w : (is_k ? ra.kn_w : nullptr);
+  // step metadata and tables (written before this step's kernel chain
+  // started -- pm_meta_upload is not a dependent launch): load ahead of the wait
+  int pos[RC];
+  float cs[RC], sn[RC];
+  int slot_off[RC];
+  const float nwd = nw ? __bfloat162float(nw[d]) : 1.f;
+#pragma unroll
+  for (int j = 0; j < RC; ++j) pos[j] = c0 + j < tok_end ? ra.positions[tok_base + c0 + j] : 0;
+#pragma unroll
+  for (int j = 0; j < RC; ++j) {
+    const int m = tok_base + c0 + j;
+    const float* t = ra.rope + (size_t)pos[j] * hd + d % half;
+    cs[j] = t[0];
+    sn[j] = t[half];
+    slot_off[j] = (!is_q && c0 + j < tok_end) ? ra.block_table[(size_t)m * ra.max_blocks + pos[j] / 16] : 0;
+  }
+  pdl_wait();
+  float v[RC];
+  if (nseg > 1) {
+    sum_partials<BN>(a, unit, nseg, c0, r, v);
+#pragma unroll
+    for (int j = 0; j < RC; ++j) v[j] = __bfloat162float(__float2bfloat16(v[j]));
+  } else {
+    const bf16* q = reinterpret_cast<const bf16*>(a.out);
+#pragma unroll
+    for (int j = 0; j < RC; ++j)
+      v[j] = (row_ok && c0 + j < tok_end) ? __bfloat162float(q[(size_t)(tok_base + c0 + j) * a.ld_out + n]) : 0.f;
+  }
+  const int wph = hd / 32;                               // warps per head
+  __shared__ float sx[RC][UNIT_ROWS];
+  __shared__ float sss[RC][8];
+  // per-head RMSNorm (q, k) over the head's hd features
+  if (nw) {
+#pragma unroll
+    for (int j = 0; j < RC; ++j) {
+      const float ss = warp_sum(v[j] * v[j]);
+      if (lane == 0) sss[j][warp] = ss;
+    }
+  }
+  __syncthreads();
+  if (nw) {
+    const int w0 = (warp / wph) * wph;
+#pragma unroll
+    for (int j = 0; j < RC; ++j) {
+      float ss = 0.f;
+      for (int w = 0; w < wph; ++w) ss += sss[j][w0 + w];
+      v[j] = v[j] * rsqrtf(ss / (float)hd + ra.eps) * nwd;
+    }
+  }
+  // rotate_half RoPE: partner of feature d is d +- hd/2 in the same head
+#pragma unroll
+  for (int j = 0; j < RC; ++j) sx[j][r] = v[j];
+  __syncthreads();
+  if (!row_ok) return;
+#pragma unroll
+  for (int j = 0; j < RC; ++j) {
+    if (c0 + j >= tok_end) continue;
+    const int m = tok_base + c0 + j;
+    float x = v[j];
+    if (is_q || is_k) {
+      const float partner = sx[j][d < half ? r + half : r - half];
+      x = d < half ? (x * cs[j] - partner * sn[j]) : (x * cs[j] + partner * sn[j]);
+    }
+    bf16* dst;
+    if (is_q) {
+      dst = ra.q_out + ((size_t)m * ra.H + hg) * hd + d;
+    } else {
+      const int kv = is_k ? 0 : 1;
+      const int g = is_k ? hg - ra.H : hg - ra.H - ra.Hkv;
+      const size_t tok_stride = (size_t)ra.L_s * 2 * ra.Hkv * hd;
+      dst = ra.pool + ((size_t)slot_off[j] * 16 + (pos[j] & 15)) * tok_stride +
+            (((size_t)ra.layer * 2 + kv) * ra.Hkv + g) * hd + d;
+    }
+    *dst = __float2bfloat16(x);
+  }
+}
+
+enum Post : int { POST_NONE = 0, POST_RESID_NORM = 1, POST_QKV_ROPE = 2 };
+
+template <int BN>
+int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int post = POST_NONE,
+           const NormArgs* na = nullptr, const RopeArgs* ra = nullptr) {
   using C = Cfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -593,8 +705,13 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st) {
     attr_set = true;
   }
   cudaError_t e = launch_k(gemm_stream_kernel<BN>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, *tx, a);
-  if (e != cudaSuccess || a.fixup || a.max_segs <= 1 || (a.debug & 1)) return (int)e;
-  return (int)launch_k(gemm_reduce_kernel<BN>, dim3(a.n_units * a.tok_tiles, BN / RC), dim3(256), 0, st, a, grid);
+  if (e != cudaSuccess) return (int)e;
+  const dim3 pg(a.n_units * a.tok_tiles, BN / RC);
+  if (post == POST_QKV_ROPE)   // every unit (whole ones read the stored bf16)
+    return (int)launch_k(gemm_qkv_rope_kernel<BN>, pg, dim3(256), 0, st, a, grid, *ra);
+  if (a.max_segs <= 1 || (a.debug & 1)) return 0;
+  if (post == POST_RESID_NORM) return (int)launch_k(gemm_resid_norm_kernel<BN>, pg, dim3(256), 0, st, a, grid, *na);
+  return (int)launch_k(gemm_reduce_kernel<BN>, pg, dim3(256), 0, st, a, grid);
 }
 
 }  // namespace
@@ -628,29 +745,102 @@ extern "C" int pm_gemm_max_segments(long long total, int kb, int grid) {
   return best;
 }
 
+// Units of a stream-K launch split across more than one CTA (host helper;
+// the per-row arrival count of pm_gemm_resid_rmsnorm).
+extern "C" int pm_gemm_split_units(long long total, int kb, int grid) {
+  int n = 0;
+  for (long long u = 0; u * kb < total; ++u) {
+    const long long first = ((u * kb + 1) * grid + total - 1) / total - 1;
+    const long long last = (((u + 1) * kb) * grid + total - 1) / total - 1;
+    n += last > first;
+  }
+  return n;
+}
+
+static int make_args(GemmArgs& a, int& grid, const void* w_packed, int n_out, int n_units, int k, int m_tok,
+                     int bn, int epilogue, void* out, int ld_out, float* ws, int max_segs, float* amax_val,
+                     int* amax_idx, int m_cap, const void* prefetch, unsigned long long prefetch_bytes) {
+  if (k % BK || m_tok < 1 || m_tok > m_cap || grid < 1) return (int)cudaErrorInvalidValue;
+  const int tok_tiles = (m_tok + bn - 1) / bn;
+  a = GemmArgs{reinterpret_cast<const uint8_t*>(w_packed), n_out, n_units, k / BK, m_tok, tok_tiles, epilogue,
+               out, ld_out, ws, max_segs, amax_val, amax_idx, m_cap,
+               reinterpret_cast<const uint8_t*>(prefetch), prefetch ? prefetch_bytes : 0ull,
+               (long long)n_units * tok_tiles * (k / BK), 0};
+  if (getenv("PM_GEMM_DEBUG")) a.debug = atoi(getenv("PM_GEMM_DEBUG"));
+  if (getenv("PM_GEMM_GRID")) grid = atoi(getenv("PM_GEMM_GRID"));  // tuning experiments only
+  if (grid > a.total) grid = (int)a.total;
+  return 0;
+}
+
+template <typename F>
+static int dispatch_bn(int bn, F&& f) {
+  switch (bn) {
+    case 16: return f(std::integral_constant<int, 16>{});
+    case 32: return f(std::integral_constant<int, 32>{});
+    case 64: return f(std::integral_constant<int, 64>{});
+    case 128: return f(std::integral_constant<int, 128>{});
+    case 256: return f(std::integral_constant<int, 256>{});
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
 // w_packed: [n_units][kb][2][128][64] bf16, each 128x64 tile in the 128B-
 // swizzled K-major UMMA smem image (see ops.pack_weight).
 extern "C" int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
                        int bn, int grid, int epilogue, void* out, int ld_out, float* ws, int max_segs,
-                       float* amax_val, int* amax_idx, int m_cap, int* counters, const void* prefetch,
+                       float* amax_val, int* amax_idx, int m_cap, const void* prefetch,
                        unsigned long long prefetch_bytes, void* stream) {
-  if (k % BK || m_tok < 1 || m_tok > m_cap || grid < 1) return (int)cudaErrorInvalidValue;
-  const int tok_tiles = (m_tok + bn - 1) / bn;
-  GemmArgs a{reinterpret_cast<const uint8_t*>(w_packed), n_out, n_units, k / BK, m_tok, tok_tiles, epilogue,
-             out, ld_out, ws, max_segs, amax_val, amax_idx, m_cap, counters,
-             reinterpret_cast<const uint8_t*>(prefetch), prefetch ? prefetch_bytes : 0ull,
-             (long long)n_units * tok_tiles * (k / BK), 0, 0};
-  if (getenv("PM_GEMM_FIXUP")) a.fixup = atoi(getenv("PM_GEMM_FIXUP"));
-  if (getenv("PM_GEMM_DEBUG")) a.debug = atoi(getenv("PM_GEMM_DEBUG"));
-  if (grid > a.total) grid = (int)a.total;
+  GemmArgs a;
+  int rc = make_args(a, grid, w_packed, n_out, n_units, k, m_tok, bn, epilogue, out, ld_out, ws, max_segs,
+                     amax_val, amax_idx, m_cap, prefetch, prefetch_bytes);
+  if (rc) return rc;
   auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   auto st = reinterpret_cast<cudaStream_t>(stream);
-  switch (bn) {
-    case 16: return launch<16>(tx, a, grid, st);
-    case 32: return launch<32>(tx, a, grid, st);
-    case 64: return launch<64>(tx, a, grid, st);
-    case 128: return launch<128>(tx, a, grid, st);
-    case 256: return launch<256>(tx, a, grid, st);
-    default: return (int)cudaErrorInvalidValue;
-  }
+  return dispatch_bn(bn, [&](auto c) { return launch<decltype(c)::value>(tx, a, grid, st); });
+}
+
+// Residual projection fused with the next RMSNorm: resid[m][0..n_out) +=
+// X W^T (fp32), then xn[m] = RMSNorm(resid[m]) * norm_w (bf16) for every
+// row.  row_counters: int[m_cap], zero at rest (left zero).  When the
+// stream-K partition splits no unit the norm runs as a separate kernel.
+extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k,
+                                     int m_tok, int bn, int grid, float* resid, float* ws, int max_segs, int m_cap,
+                                     const void* prefetch, unsigned long long prefetch_bytes, const void* norm_w,
+                                     void* xn, float eps, int* row_counters, void* stream) {
+  GemmArgs a;
+  int rc = make_args(a, grid, w_packed, n_out, n_units, k, m_tok, bn, EPI_RESID_ADD_F32, resid, n_out, ws,
+                     max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes);
+  if (rc) return rc;
+  if (n_out % 8 || n_out > 256 * 4 * NORM_V4) return (int)cudaErrorInvalidValue;
+  NormArgs na{reinterpret_cast<const bf16*>(norm_w), reinterpret_cast<bf16*>(xn), row_counters,
+              pm_gemm_split_units(a.total, a.kb, grid), eps};
+  auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  const int post = (na.n_split > 0 && !(a.debug & 1)) ? POST_RESID_NORM : POST_NONE;
+  rc = dispatch_bn(bn, [&](auto c) { return launch<decltype(c)::value>(tx, a, grid, st, post, &na); });
+  if (rc || post == POST_RESID_NORM) return rc;
+  return launch_rmsnorm(resid, norm_w, xn, m_tok, n_out, eps, st);
+}
+
+// QKV projection fused with (Qwen3 q/k RMSNorm) + rotate-half RoPE + paged KV
+// append: q_out[m][H][hd] and the pool slot of positions[m] in layer `layer`
+// (same contract as pm_qkv_rope_append).  qkv_out [m_cap][n_out] bf16 is
+// scratch for units the partition leaves whole.
+extern "C" int pm_gemm_qkv_rope(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
+                                int bn, int grid, void* qkv_out, float* ws, int max_segs, int m_cap,
+                                const void* prefetch, unsigned long long prefetch_bytes, void* q_out, void* pool,
+                                const int* block_table, const int* positions, const float* rope, const void* qn_w,
+                                const void* kn_w, int H, int Hkv, int hd, int layer, int L_s, int max_blocks,
+                                float eps, void* stream) {
+  GemmArgs a;
+  int rc = make_args(a, grid, w_packed, n_out, n_units, k, m_tok, bn, EPI_STORE_BF16, qkv_out, n_out, ws,
+                     max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes);
+  if (rc) return rc;
+  if (n_out != (H + 2 * Hkv) * hd || (hd != 64 && hd != 128) || UNIT_ROWS % hd) return (int)cudaErrorInvalidValue;
+  RopeArgs ra{reinterpret_cast<bf16*>(q_out), reinterpret_cast<bf16*>(pool), block_table, positions, rope,
+              reinterpret_cast<const bf16*>(qn_w), reinterpret_cast<const bf16*>(kn_w), H, Hkv, hd, layer, L_s,
+              max_blocks, eps};
+  auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  return dispatch_bn(bn, [&](auto c) { return launch<decltype(c)::value>(tx, a, grid, st, POST_QKV_ROPE, nullptr, &ra); });
 }

@@ -115,12 +115,15 @@ def gemm_plan(n_units: int, kb: int, m_tok: int, sms: int = SMS):
     tt = -(-m_tok // bn)
     total = n_units * tt * kb
     grid = min(sms, total)
+    import os
+    if os.environ.get("PM_GEMM_GRID"):  # tuning experiments only (must match the library's override)
+        grid = min(int(os.environ["PM_GEMM_GRID"]), total)
     segs = _C.lib().pm_gemm_max_segments(total, kb, grid)
     return bn, grid, segs, tt
 
 
 class GemmWorkspace:
-    """Stream-K partials, per-unit counters and argmax partials shared by all
+    """Stream-K partials, per-row counters and argmax partials shared by all
     projections of one executor (launches on one stream run in order)."""
 
     def __init__(self, m_cap: int, ws_floats: int, max_units: int, vocab_units: int, device):
@@ -128,9 +131,8 @@ class GemmWorkspace:
         self.ws = torch.empty(max(1, ws_floats), dtype=torch.float32, device=device)
         self.amax_val = torch.empty(max(1, vocab_units) * m_cap, dtype=torch.float32, device=device)
         self.amax_idx = torch.empty(max(1, vocab_units) * m_cap, dtype=torch.int32, device=device)
-        # stream-K fixup arrive/leave counters per (unit, token tile); kernels leave them zero
-        self.counters = torch.zeros(2 * max(1, max_units, vocab_units) * (-(-m_cap // 256)), dtype=torch.int32,
-                                    device=device)
+        # per-row arrival counts of the fused residual + RMSNorm epilogue; kernels leave them zero
+        self.row_cnt = torch.zeros(m_cap, dtype=torch.int32, device=device)
 
     @staticmethod
     def floats_needed(linears, m_cap):
@@ -164,25 +166,57 @@ class Linear:
             p = self._plans[m_tok] = gemm_plan(self.n_units, self.kb, m_tok)
         return p
 
+    @staticmethod
+    def _pf(prefetch):
+        return (None, 0) if prefetch is None else (C.c_void_p(prefetch[0].data_ptr()), int(prefetch[1]))
+
+    def _timed(self, kind_bytes, stream, go):
+        if TIMER is None:
+            go()
+        else:
+            TIMER.around("gemm", kind_bytes, stream, go)
+
     def __call__(self, x_maps: dict, m_tok: int, epilogue: int, out, ld_out: int, ws: GemmWorkspace,
                  stream=None, prefetch=None):
         """``prefetch``: optional (tensor, nbytes) the next operation reads
         first; the kernel pulls it into L2 while it drains."""
         bn, grid, segs, tt = self.plan(m_tok)
-        pf_ptr, pf_bytes = (None, 0) if prefetch is None else (C.c_void_p(prefetch[0].data_ptr()), int(prefetch[1]))
+        pf_ptr, pf_bytes = self._pf(prefetch)
 
         def go():
             _C.call("pm_gemm", _ptr(self.packed), x_maps[bn].ptr, self.n_out, self.n_units, self.k, m_tok, bn,
                     grid, epilogue, _ptr(out), ld_out, _ptr(ws.ws), segs,
-                    _ptr(ws.amax_val), _ptr(ws.amax_idx), ws.m_cap, _ptr(ws.counters), pf_ptr, pf_bytes,
-                    _stream(stream))
-        if TIMER is None:
-            go()
-        else:
-            out_b = {EPI_STORE_BF16: 2, EPI_RESID_ADD: 8, EPI_SILU_MUL: 1,
-                     EPI_LOGITS_ARGMAX: 4 if out is not None else 0}[epilogue]
-            nbytes = self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * out_b
-            TIMER.around("gemm", nbytes, stream, go)
+                    _ptr(ws.amax_val), _ptr(ws.amax_idx), ws.m_cap, pf_ptr, pf_bytes, _stream(stream))
+        out_b = {EPI_STORE_BF16: 2, EPI_RESID_ADD: 8, EPI_SILU_MUL: 1,
+                 EPI_LOGITS_ARGMAX: 4 if out is not None else 0}[epilogue]
+        self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * out_b, stream, go)
+
+    def resid_rmsnorm(self, x_maps: dict, m_tok: int, resid, ws: GemmWorkspace, norm_w, xn, eps: float,
+                      stream=None, prefetch=None):
+        """resid += x W^T, then xn = RMSNorm(resid) * norm_w -- the residual
+        projection fused with the next layer norm (pm_gemm_resid_rmsnorm)."""
+        bn, grid, segs, tt = self.plan(m_tok)
+        pf_ptr, pf_bytes = self._pf(prefetch)
+
+        def go():
+            _C.call("pm_gemm_resid_rmsnorm", _ptr(self.packed), x_maps[bn].ptr, self.n_out, self.n_units, self.k,
+                    m_tok, bn, grid, _ptr(resid), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, _ptr(norm_w),
+                    _ptr(xn), float(eps), _ptr(ws.row_cnt), _stream(stream))
+        self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * (8 + 4 + 2), stream, go)
+
+    def qkv_rope(self, x_maps: dict, m_tok: int, qkv, ws: GemmWorkspace, q_out, pool, block_table, positions,
+                 rope, qn_w, kn_w, H, Hkv, hd, layer, L_s, eps, stream=None, prefetch=None):
+        """QKV projection fused with q/k RMSNorm + RoPE + paged KV append
+        (pm_gemm_qkv_rope); ``qkv`` is scratch for units left whole."""
+        bn, grid, segs, tt = self.plan(m_tok)
+        pf_ptr, pf_bytes = self._pf(prefetch)
+
+        def go():
+            _C.call("pm_gemm_qkv_rope", _ptr(self.packed), x_maps[bn].ptr, self.n_out, self.n_units, self.k,
+                    m_tok, bn, grid, _ptr(qkv), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, _ptr(q_out),
+                    _ptr(pool), _ptr(block_table), _ptr(positions), _ptr(rope), _ptr(qn_w), _ptr(kn_w), H, Hkv,
+                    hd, layer, L_s, block_table.shape[1], float(eps), _stream(stream))
+        self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * 2, stream, go)
 
 
 def activation_maps(buf: torch.Tensor) -> dict:

@@ -116,19 +116,26 @@ class StageExecutor:
             return
         if self.first:
             ops.embed(self.tok_table, self.slots, self.embed, self.resid, M, stream)
+        # the stage's first norm; every later norm is fused into the residual
+        # projection that precedes it (pm_gemm_resid_rmsnorm)
+        ops.rmsnorm(self.resid, self.W[0]["attn_norm"], self.xn, M, s.eps, stream)
         for li, w in enumerate(self.W):
-            ops.rmsnorm(self.resid, w["attn_norm"], self.xn, M, s.eps, stream)
-            w["qkv"](self.xn_maps, M, ops.EPI_STORE_BF16, self.qkv, s.qkv_out, self.gws, stream)
-            ops.qkv_rope_append(self.qkv, self.q, self.pool, self.block_table, self.positions, self.rope,
-                                w["q_norm"], w["k_norm"], M, s.H, s.Hkv, s.hd, li, self.L_s, s.eps, stream)
+            # QKV projection + q/k norm + RoPE + paged KV append (one fused epilogue)
+            w["qkv"].qkv_rope(self.xn_maps, M, self.qkv, self.gws, self.q, self.pool, self.block_table,
+                              self.positions, self.rope, w["q_norm"], w["k_norm"], s.H, s.Hkv, s.hd, li, self.L_s,
+                              s.eps, stream)
             ops.paged_attention(self.pool_map, self.q, self.block_table, self.seq_lens, self.attn, self.aws,
                                 M, s.H, s.Hkv, s.hd, li, self.L_s, stream, kv_tokens=kv_tokens)
-            w["o"](self.attn_maps, M, ops.EPI_RESID_ADD, self.resid, s.d, self.gws, stream)
-            ops.rmsnorm(self.resid, w["mlp_norm"], self.xn, M, s.eps, stream)
+            # O projection + residual + post-attention RMSNorm
+            w["o"].resid_rmsnorm(self.attn_maps, M, self.resid, self.gws, w["mlp_norm"], self.xn, s.eps, stream)
             w["gu"](self.xn_maps, M, ops.EPI_SILU_MUL, self.act, s.ffn, self.gws, stream)
-            w["down"](self.act_maps, M, ops.EPI_RESID_ADD, self.resid, s.d, self.gws, stream)
+            # down projection + residual + the next norm (next layer's, or the final one)
+            nxt = self.W[li + 1]["attn_norm"] if li + 1 < len(self.W) else (self.final_norm if self.last else None)
+            if nxt is not None:
+                w["down"].resid_rmsnorm(self.act_maps, M, self.resid, self.gws, nxt, self.xn, s.eps, stream)
+            else:
+                w["down"](self.act_maps, M, ops.EPI_RESID_ADD, self.resid, s.d, self.gws, stream)
         if self.last:
-            ops.rmsnorm(self.resid, self.final_norm, self.xn, M, s.eps, stream)
             self.lm_head(self.xn_maps, M, ops.EPI_LOGITS_ARGMAX, self.logits, s.vocab, self.gws, stream)
             ops.argmax_reduce(self.gws, self.lm_head.n_units, M, self.out_ids, self.tok_table, self.slots, stream)
 
@@ -154,14 +161,17 @@ class StageExecutor:
         return g
 
     def kernels_per_step(self, M: int = None) -> int:
-        """Kernels of one forward(M): embed, per layer 2 rmsnorm + rope/append +
-        attention + 4 projections (each 1-2 launches), final norm + lm_head +
-        argmax."""
+        """Kernels of one forward(M): embed, the first RMSNorm, per layer the
+        fused QKV (GEMM + norm/RoPE/append kernel), attention, the fused O and
+        down projections (GEMM + reduce/residual/RMSNorm kernel each) and the
+        gate/up GEMM (1-2 launches); lm_head (1-2) + argmax."""
         M = M or self.m_cap
-        n = (1 if self.first else 0) + 4 * self.L_s
-        n += sum(w[k].launches(M) for w in self.W for k in ("qkv", "o", "gu", "down"))
-        if self.last:
-            n += 2 + self.lm_head.launches(M)
+        n = (1 if self.first else 0) + 1 + self.L_s * (2 + 1 + 2 + 2)
+        n += sum(w["gu"].launches(M) for w in self.W)
+        if not self.last:
+            n += self.W[-1]["down"].launches(M) - 2
+        else:
+            n += 1 + self.lm_head.launches(M)
         return n
 
     # ------------------------------------------------------------------ roofline

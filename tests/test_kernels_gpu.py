@@ -50,8 +50,6 @@ def test_gemm_store_and_resid(n_out, k, m):
         lin(maps, 1, ops.EPI_STORE_BF16, y1, n_out, ws)
         torch.cuda.synchronize()
         assert torch.equal(y1[0], y[0])
-    # the in-kernel stream-K fixup re-arms its counters for the next launch
-    assert (ws.counters == 0).all()
 
 
 def test_gemm_silu_mul_interleaved():
@@ -182,3 +180,76 @@ def test_rope_append_and_paged_attention(spec):
         np.testing.assert_allclose(got, want, atol=2e-2, rtol=2e-2, err_msg=f"row {r} len {L}")
     # untouched layers / slots stay zero
     assert np.all(Pn[:, :, 0] == 0) and np.all(Pn[:, :, 2] == 0)
+
+
+@pytest.mark.parametrize("n_out,k,m", [(4096, 4096, 128), (512, 256, 7), (8192, 1024, 200), (512, 64, 16),
+                                       (4096, 12288, 64)])
+def test_fused_resid_rmsnorm_matches_unfused(n_out, k, m):
+    """pm_gemm_resid_rmsnorm == pm_gemm(+resid) then pm_rmsnorm: the residual
+    bit-for-bit, the normalised row bit-for-bit (same reduction order), and
+    the per-row arrival counters re-armed; (512, 64) splits no unit and takes
+    the separate-norm path."""
+    g = torch.Generator(device=DEV).manual_seed(n_out + k + m)
+    w = (torch.randn(n_out, k, generator=g, device=DEV) * 0.05).to(torch.bfloat16)
+    m_cap = max(256, m)
+    x = torch.zeros(m_cap, k, device=DEV, dtype=torch.bfloat16)
+    x[:m] = torch.randn(m, k, generator=g, device=DEV).to(torch.bfloat16)
+    nw = (1 + 0.1 * torch.randn(n_out, generator=g, device=DEV)).to(torch.bfloat16)
+    lin = ops.Linear(w)
+    maps = ops.activation_maps(x)
+    ws = _ws(m_cap, lin)
+    r0 = torch.randn(m_cap, n_out, generator=g, device=DEV)
+    r_ref, r_fused = r0.clone(), r0.clone()
+    xn_ref = torch.zeros(m_cap, n_out, device=DEV, dtype=torch.bfloat16)
+    xn_fused = torch.zeros_like(xn_ref)
+    lin(maps, m, ops.EPI_RESID_ADD, r_ref, n_out, ws)
+    ops.rmsnorm(r_ref, nw, xn_ref, m, 1e-6)
+    lin.resid_rmsnorm(maps, m, r_fused, ws, nw, xn_fused, 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(r_fused, r_ref)
+    assert torch.equal(xn_fused[:m], xn_ref[:m])
+    assert (ws.row_cnt == 0).all()
+
+
+@pytest.mark.parametrize("H,Hkv,hd,k,m,qk_norm", [(32, 8, 128, 4096, 128, True), (8, 2, 64, 256, 5, True),
+                                                 (600, 20, 64, 128, 40, False)])
+def test_fused_qkv_rope_matches_unfused(H, Hkv, hd, k, m, qk_norm):
+    """pm_gemm_qkv_rope == pm_gemm(store bf16) then pm_qkv_rope_append: q and
+    the appended K/V agree to one bf16 rounding (the per-head norm sums in a
+    different order); (600, 20, 64, k=128) leaves units whole."""
+    g = torch.Generator(device=DEV).manual_seed(H + k + m)
+    n_out = (H + 2 * Hkv) * hd
+    w = (torch.randn(n_out, k, generator=g, device=DEV) * 0.05).to(torch.bfloat16)
+    m_cap = 256
+    x = torch.zeros(m_cap, k, device=DEV, dtype=torch.bfloat16)
+    x[:m] = torch.randn(m, k, generator=g, device=DEV).to(torch.bfloat16)
+    lin = ops.Linear(w)
+    maps = ops.activation_maps(x)
+    ws = _ws(m_cap, lin)
+    L_s, layer, max_blocks = 2, 1, 8
+    n_blocks = m * 4 + 4
+    pool_ref = torch.zeros(n_blocks * 16 * L_s * 2 * Hkv * hd, dtype=torch.bfloat16, device=DEV)
+    pool_fused = torch.zeros_like(pool_ref)
+    bt = torch.randperm(n_blocks, generator=torch.Generator().manual_seed(m))[: m * 4].view(m, 4).to(torch.int32)
+    btab = torch.zeros(m, max_blocks, dtype=torch.int32)
+    btab[:, :4] = bt
+    btab = btab.to(DEV)
+    pos = torch.randint(0, 64, (m,), generator=torch.Generator().manual_seed(k)).to(torch.int32).to(DEV)
+    spec_rope = torch.randn(128, hd, generator=g, device=DEV)
+    qn = kn = None
+    if qk_norm:
+        qn = (1 + 0.1 * torch.randn(hd, generator=g, device=DEV)).to(torch.bfloat16)
+        kn = (1 + 0.1 * torch.randn(hd, generator=g, device=DEV)).to(torch.bfloat16)
+    qkv = torch.zeros(m_cap, n_out, device=DEV, dtype=torch.bfloat16)
+    q_ref = torch.zeros(m, H, hd, device=DEV, dtype=torch.bfloat16)
+    q_fused = torch.zeros_like(q_ref)
+    lin(maps, m, ops.EPI_STORE_BF16, qkv, n_out, ws)
+    ops.qkv_rope_append(qkv, q_ref, pool_ref, btab, pos, spec_rope, qn, kn, m, H, Hkv, hd, layer, L_s, 1e-6)
+    scratch = torch.zeros_like(qkv)
+    lin.qkv_rope(maps, m, scratch, ws, q_fused, pool_fused, btab, pos, spec_rope, qn, kn, H, Hkv, hd, layer, L_s,
+                 1e-6)
+    torch.cuda.synchronize()
+    tol = 2 ** -7  # one bf16 rounding step (relative)
+    assert torch.allclose(q_fused.float(), q_ref.float(), atol=tol * q_ref.abs().max().item(), rtol=tol)
+    assert torch.allclose(pool_fused.float(), pool_ref.float(), atol=tol * pool_ref.abs().max().item(), rtol=tol)
+    assert (pool_fused != 0).sum() == (pool_ref != 0).sum()
