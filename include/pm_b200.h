@@ -43,6 +43,10 @@ int pm_meta_upload(int count, void* const* dst, const void* const* src, const in
 int pm_copy_pieces(void* dst_base, const void* src_base, const long long* dst_off, const long long* src_off,
                    int n, unsigned long long bytes, void* stream);
 
+/* pitched copy (one layer's K/V of a run of tokens, pool <-> host replica; prefill offload) */
+int pm_copy_2d(void* dst, unsigned long long dpitch, const void* src, unsigned long long spitch,
+               unsigned long long width, unsigned long long height, void* stream);
+
 /* ---- per-stage decode forward ---------------------------------------------- */
 int pm_embed(const int* tok_table, const int* slots, const void* table, float* resid, int M, int d,
              void* stream);

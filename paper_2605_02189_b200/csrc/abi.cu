@@ -43,6 +43,16 @@ extern "C" int pm_tmap_encode_2d(void* tmap_out, const void* gaddr, unsigned lon
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
+// Pitched copy (cudaMemcpy2DAsync): `height` rows of `width` bytes, row
+// strides dpitch / spitch -- one layer's K/V of a run of tokens between the
+// pool and the host replica (token stride = the pitch).
+extern "C" int pm_copy_2d(void* dst, unsigned long long dpitch, const void* src, unsigned long long spitch,
+                          unsigned long long width, unsigned long long height, void* stream) {
+  if (height == 0) return 0;
+  return (int)cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault,
+                                reinterpret_cast<cudaStream_t>(stream));
+}
+
 // Pinned, portable host memory for the KV host replica (the paper's "CPU KV
 // pool").  The caller owns it and frees it with pm_host_free.
 extern "C" int pm_host_alloc(unsigned long long bytes, void** out) {

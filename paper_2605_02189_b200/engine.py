@@ -81,10 +81,11 @@ class DecodeEngine:
                  requests: dict, *, pp: int = 1, device="cuda", mode="dynamic", quota_tokens=0,
                  seed: int = 0, m_cap: int = None, timing=True, kv_init="random", prompts=None,
                  record_logits=False, max_pos=None, trace: EventTrace = None, graphs: bool = True,
-                 local_stages=None):
+                 local_stages=None, staging_pool_requests: int = 2):
         """``local_stages``: which of the ``pp`` stages this process hosts
         (default all; one rank per stage under torchrun, see pipeline.py)."""
         self.spec, self.cfg, self.params = spec, cfg, params
+        self.staging_pool_requests = staging_pool_requests
         self.requests = requests
         self.dev = torch.device(device)
         self.metrics = EpisodeMetrics()
@@ -148,6 +149,8 @@ class DecodeEngine:
             assert prompts is not None
             self._prefill(prompts)
             return
+        if how == "none":   # caller fills the KV (prefill.run_prefill)
+            return
         # timing runs: random KV in HBM for resident blocks; the host replica
         # keeps whatever the fresh pinned pages hold (zeros) -- values do not
         # change the timing
@@ -159,60 +162,13 @@ class DecodeEngine:
         torch.cuda.synchronize()
 
     def _prefill(self, prompts):
-        """Prefill by teacher-forced decode steps through the same kernels
-        (SURVEY.md 8f row 1 is the real prefill path; this seeds parity runs).
-        Each request's prompt KV is written to scratch blocks, copied to its
-        host replica region, and resident requests' blocks are then filled
-        from the host copy like any prefetch."""
-        rids = sorted(self.requests)
-        free = sorted(set(range(self.control.alloc.total)) -
-                      {b for t in self.control.alloc.tables.values() for b in t})
-        # groups of requests that fit the scratch blocks and m_cap rows
-        groups, cur, used = [], [], 0
-        for rid in rids:
-            need = blocks_for_tokens(len(prompts[rid]), 16)
-            if cur and (used + need > len(free) or len(cur) >= self.m_cap):
-                groups.append(cur)
-                cur, used = [], 0
-            cur.append(rid)
-            used += need
-        if cur:
-            groups.append(cur)
-        for group in groups:
-            tables, k = {}, 0
-            for rid in group:
-                need = blocks_for_tokens(len(prompts[rid]), 16)
-                tables[rid] = free[k:k + need]
-                k += need
-            P = max(len(prompts[r]) for r in group)
-            for p in range(P):
-                rows = [r for r in group if p < len(prompts[r])]
-                ex0, kv0 = self.stages[0]
-                with torch.cuda.stream(kv0.compute):
-                    tok = torch.tensor([int(prompts[r][p]) for r in rows], dtype=torch.int32)
-                    idx = torch.tensor([self.slot_of[r] for r in rows])
-                    ex0.tok_table[idx.to(self.dev)] = tok.to(self.dev)
-                self._upload_meta(rows, [p] * len(rows), tables)
-                self._forward_all(len(rows))
-            torch.cuda.synchronize()
-            for ex, kv in self.stages:
-                host = kv.rep.as_tensor()
-                pv = ex.pool.view(torch.uint8).view(ex.pool_blocks, ex.block_bytes)
-                for rid in group:
-                    off = kv.rep.offset(self.slot_of[rid])
-                    for lb, pb in enumerate(tables[rid]):
-                        host[off + lb * ex.block_bytes: off + (lb + 1) * ex.block_bytes].copy_(pv[pb].cpu())
-        # first generated token came out of the last prompt step; move it to stage 0
-        if len(self.stages) > 1:
-            self.stages[0][0].tok_table.copy_(self.stages[-1][0].tok_table)
-        for ex, kv in self.stages:
-            host = kv.rep.as_tensor()
-            pv = ex.pool.view(torch.uint8).view(ex.pool_blocks, ex.block_bytes)
-            for rid, blocks in self.control.alloc.tables.items():
-                off = kv.rep.offset(self.slot_of[rid])
-                for lb, pb in enumerate(blocks):
-                    pv[pb].copy_(host[off + lb * ex.block_bytes: off + (lb + 1) * ex.block_bytes].to(self.dev))
-        torch.cuda.synchronize()
+        """Real prefill of every request (chunked, layer-wise async KV offload
+        to the host replicas, bounded staging -- prefill.PrefillRunner, REF
+        pipeline_sim.py:241-323).  Resident requests end with their KV in
+        their own blocks and on the host; the others on the host only."""
+        from .prefill import PrefillRunner
+        self.prefill_runner = PrefillRunner(self, staging_pool_requests=self.staging_pool_requests)
+        self.prefill_trace, self.prefill_makespan = self.prefill_runner.run(prompts)
 
     # ------------------------------------------------------------------ per step
     def bucket(self, M):
@@ -221,14 +177,26 @@ class DecodeEngine:
     def _upload_meta(self, rows, positions, tables, stream=None):
         """Block tables, positions, seq lens and slots of the step's rows,
         padded to the 16-row bucket with rows aimed at the trash block/slot."""
-        n, mb = len(rows), self.max_blocks
+        self._fill_meta([tables[r] for r in rows], positions, [self.slot_of[r] for r in rows], stream)
+
+    def _upload_meta_rows(self, table, positions, M=None, last_slot=None, stream=None):
+        """Prefill chunk: every row is a token of one request (its block
+        table); greedy ids go to the trash slot except the last row's, which
+        goes to ``last_slot`` when given (the request's first generated token)."""
+        n = len(positions)
+        slots = [self.trash_slot] * n
+        if last_slot is not None:
+            slots[-1] = last_slot
+        self._fill_meta([table] * n, positions, slots, stream)
+
+    def _fill_meta(self, row_tables, positions, slots, stream=None):
+        n, mb = len(row_tables), self.max_blocks
         M = self.bucket(n)
         k, buf = self.meta.next()
         a = buf.numpy()
         bt = a[:M * mb].reshape(M, mb)
         bt[:] = 0
-        for i, r in enumerate(rows):
-            tb = tables[r]
+        for i, tb in enumerate(row_tables):
             bt[i, :len(tb)] = tb
         bt[n:, 0] = self.trash_block
         o = M * mb
@@ -236,7 +204,7 @@ class DecodeEngine:
         a[o + n:o + M] = 0
         a[o + M:o + M + n] = np.asarray(positions) + 1
         a[o + M + n:o + 2 * M] = 1
-        a[o + 2 * M:o + 2 * M + n] = [self.slot_of[r] for r in rows]
+        a[o + 2 * M:o + 2 * M + n] = slots
         a[o + 2 * M + n:o + 3 * M] = self.trash_slot
         # attention work list (chunk-major) over the bucket's rows, padding rows included
         wo = o + 3 * M

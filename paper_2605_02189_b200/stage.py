@@ -84,6 +84,7 @@ class StageExecutor:
         self.slots = torch.zeros(m_cap, dtype=i32, device=device)
         self.meta_dev = [self.block_table, self.positions, self.seq_lens, self.slots]
         self.tok_table = torch.zeros(n_slots, dtype=i32, device=device)
+        self.prefill_tokens = torch.zeros(m_cap, dtype=i32, device=device)
         self.out_ids = torch.zeros(m_cap, dtype=i32, device=device)
         self.logits = None
         self.graphs = {}
@@ -105,7 +106,7 @@ class StageExecutor:
             self.logits = torch.zeros(self.m_cap, self.spec.vocab, dtype=torch.float32, device=self.dev)
 
     # ------------------------------------------------------------------ forward
-    def forward(self, M: int, stream=None, kv_tokens: int = 0):
+    def forward(self, M: int, stream=None, kv_tokens: int = 0, prefill_tokens: bool = False, layer_hook=None):
         """One micro-batch step of M rows (metadata already on the device).
 
         Stage 0 embeds ``tok_table[slots]``; later stages expect ``resid`` to
@@ -115,7 +116,10 @@ class StageExecutor:
         if M == 0:
             return
         if self.first:
-            ops.embed(self.tok_table, self.slots, self.embed, self.resid, M, stream)
+            if prefill_tokens:   # prompt chunk: row m embeds prefill_tokens[m]
+                ops.embed(self.prefill_tokens, None, self.embed, self.resid, M, stream)
+            else:
+                ops.embed(self.tok_table, self.slots, self.embed, self.resid, M, stream)
         # the stage's first norm; every later norm is fused into the residual
         # projection that precedes it (pm_gemm_resid_rmsnorm)
         ops.rmsnorm(self.resid, self.W[0]["attn_norm"], self.xn, M, s.eps, stream)
@@ -124,6 +128,8 @@ class StageExecutor:
             w["qkv"].qkv_rope(self.xn_maps, M, self.qkv, self.gws, self.q, self.pool, self.block_table,
                               self.positions, self.rope, w["q_norm"], w["k_norm"], s.H, s.Hkv, s.hd, li, self.L_s,
                               s.eps, stream)
+            if layer_hook is not None:   # layer li's K/V is in the pool (prefill offload)
+                layer_hook(li)
             ops.paged_attention(self.pool_map, self.q, self.block_table, self.seq_lens, self.attn, self.aws,
                                 M, s.H, s.Hkv, s.hd, li, self.L_s, stream, kv_tokens=kv_tokens)
             # O projection + residual + post-attention RMSNorm
