@@ -341,6 +341,14 @@ def run_ours(args):
                                    "steps of the same run launched eagerly (the timed region replays CUDA "
                                    "graphs); achieved = algorithmic bytes per launch (GEMM: weights once + "
                                    "activations; attention: the micro-batch's KV once) / launch time"}
+    if rank == 0 and args.calibrate:
+        # on-box fit of the planner's estimator (REF model_core.py:158-182) from
+        # measured iterations of this engine; reported beside the analytic one
+        # the bench plans with (timing engine: it overwrites sampled KV slots)
+        from paper_2605_02189_b200.calibrate import calibrate_on_device, params_dict
+        cp, samples, err = calibrate_on_device(eng, reps=3)
+        out["estimator"] = {"planned_with": params_dict(params), "calibrated": params_dict(cp),
+                            "max_rel_fit_err": err, "samples": len(samples)}
     if rank == 0 and not args.no_cpu_baseline:
         kv_ctx = int(np.mean([eng.control.state.lengths.get(r, 0) for r in range(len(reqs))]))
         M = int(round(tokens / args.steps))
@@ -388,6 +396,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-kernel-timing", dest="kernel_timing", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-calibrate", dest="calibrate", action="store_false")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference"
     if args.impl == "reference":
