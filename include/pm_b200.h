@@ -51,27 +51,33 @@ int pm_copy_2d(void* dst, unsigned long long dpitch, const void* src, unsigned l
 int pm_embed(const int* tok_table, const int* slots, const void* table, float* resid, int M, int d,
              void* stream);
 int pm_rmsnorm(const float* x, const void* w, void* y, int M, int d, float eps, void* stream);
-/* stream-K tcgen05 GEMM over a packed weight ([units][K/64][2][128][64], 128B-swizzled) */
+/* stream-K tcgen05 GEMM over a packed weight ([units][K/64][2][128][64], 128B-swizzled).  grid = CTAs.
+ * cta_pair = 0: one CTA per stream-K worker computes whole 256-row units, tmap_x box [bn rows x 64];
+ * cta_pair = 1: each worker is a (2,1,1) cluster (grid even), one 128-row half per CTA, tmap_x box
+ * [bn/2 rows x 64] (each CTA loads half the activation tile and multicasts it to its partner).
+ * max_segs = pm_gemm_max_segments(total, kb, workers); the argmax epilogue writes 2 tiles (128-row
+ * halves) per 256-row unit. */
 int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok, int bn,
-            int grid, int epilogue, void* out, int ld_out, float* ws, int max_segs, float* amax_val,
+            int grid, int cta_pair, int epilogue, void* out, int ld_out, float* ws, int max_segs, float* amax_val,
             int* amax_idx, int m_cap, const void* prefetch, unsigned long long prefetch_bytes, void* stream);
 /* prefetch/prefetch_bytes: optional region the NEXT operation reads first; it is pulled into L2 while
  * this GEMM drains (keeps HBM busy across the kernel boundary); NULL/0 for none. */
 /* residual projection (O / down) fused with the next RMSNorm: resid += X W^T (fp32), then
  * xn = RMSNorm(resid) * norm_w (bf16) per row; row_counters int[m_cap], zero at rest, left zero */
 int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
-                          int bn, int grid, float* resid, float* ws, int max_segs, int m_cap, const void* prefetch,
+                          int bn, int grid, int cta_pair, float* resid, float* ws, int max_segs, int m_cap, const void* prefetch,
                           unsigned long long prefetch_bytes, const void* norm_w, void* xn, float eps,
                           int* row_counters, void* stream);
 /* QKV projection fused with (Qwen3 q/k RMSNorm) + RoPE + paged KV append (pm_qkv_rope_append's contract);
  * qkv_out [m_cap][n_out] bf16 is scratch */
 int pm_gemm_qkv_rope(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok, int bn,
-                     int grid, void* qkv_out, float* ws, int max_segs, int m_cap, const void* prefetch,
+                     int grid, int cta_pair, void* qkv_out, float* ws, int max_segs, int m_cap, const void* prefetch,
                      unsigned long long prefetch_bytes, void* q_out, void* pool, const int* block_table,
                      const int* positions, const float* rope, const void* qn_w, const void* kn_w, int H, int Hkv,
                      int hd, int layer, int L_s, int max_blocks, float eps, void* stream);
-int pm_gemm_split_units(long long total, int kb, int grid);
-int pm_gemm_max_segments(long long total, int kb, int grid);
+/* stream-K geometry helpers over `workers` (= grid, or grid / 2 in pair mode) */
+int pm_gemm_split_units(long long total, int kb, int workers);
+int pm_gemm_max_segments(long long total, int kb, int workers);
 int pm_qkv_rope_append(const void* qkv, void* q_out, void* pool, const int* block_table, const int* positions,
                        const float* rope, const void* qn_w, const void* kn_w, int M, int H, int Hkv, int hd,
                        int layer, int L_s, int max_blocks, float eps, void* stream);

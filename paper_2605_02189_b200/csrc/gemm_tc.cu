@@ -1,8 +1,11 @@
 // Decode projection GEMM on 5th-gen tensor cores (tcgen05 + TMEM), persistent
 // stream-K, weights streamed as pre-packed contiguous chunks.
 //
-// Swap-AB: a 256-row weight unit (two 128-row UMMA tiles) is the MMA "A"
-// operand and the micro-batch tokens are the MMA "N" (16..256):
+// Swap-AB: a 256-row weight unit is the MMA "A" operand and the micro-batch
+// tokens are the MMA "N" (16..256), computed by a 2-CTA cluster (one 128-row
+// UMMA tile per CTA; each CTA loads half of the activation tile and
+// multicasts it to both, so activation traffic stays one tile per unit while
+// every CTA's stream-K partial is 128 rows and there are 74 workers):
 //     D^T[n_out, tok] = W[n_out, K] . X[tok, K]^T      (fp32 in TMEM)
 // At decode batch sizes (M_tok <~ 255) the GEMM is weight-bandwidth bound, so
 // the design goal is to keep all 148 SMs streaming weights from HBM at the
@@ -54,7 +57,7 @@ struct GemmArgs {
   int ld_out;
   float* ws;          // [units*tok_tiles][max_segs][BN][256] fp32 partials of split units
   int max_segs;
-  float* amax_val;    // [units][m_cap]
+  float* amax_val;    // [units * 2 halves][m_cap]
   int* amax_idx;
   int m_cap;
   const uint8_t* pf;  // bytes the NEXT operation streams first: prefetched into L2 during this tail
@@ -63,13 +66,16 @@ struct GemmArgs {
   int debug;          // profiling only: bit0 skip epilogue math, bit2 skip partial stores, bit3 trace
 };
 
-template <int BN>
+// NH = 128-row halves of the 256-row unit one CTA computes: 2 (a CTA owns the
+// unit) or 1 (a 2-CTA cluster owns it; the X tile is split and multicast).
+template <int BN, int NH>
 struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
-  static constexpr int ACC_BUFS = BN <= 128 ? 2 : 1;            // 2 bufs x 2 halves x BN <= 512 cols
-  static constexpr int TMEM_COLS = ACC_BUFS * 2 * BN <= 32 ? 32 : (ACC_BUFS * 2 * BN <= 64 ? 64 : (ACC_BUFS * 2 * BN <= 128 ? 128 : (ACC_BUFS * 2 * BN <= 256 ? 256 : 512)));
+  static constexpr int STAGE = NH * SUB_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+  static constexpr int ACC_COLS = NH * BN;                       // one accumulator buffer
+  static constexpr int ACC_BUFS = 2 * ACC_COLS <= 512 ? 2 : 1;
+  static constexpr int TMEM_COLS = ACC_BUFS * ACC_COLS <= 32 ? 32 : (ACC_BUFS * ACC_COLS <= 64 ? 64 : (ACC_BUFS * ACC_COLS <= 128 ? 128 : (ACC_BUFS * ACC_COLS <= 256 ? 256 : 512)));
   static constexpr int SMEM = STAGES * STAGE + 1024 + 512 + 4 * BN * 8;
 };
 
@@ -94,9 +100,9 @@ struct Seg {
 };
 
 // i-th segment of this CTA; returns false when past the end
-PM_DEV bool get_seg(const GemmArgs& a, long long lo, long long hi, int i, Seg& s) {
+PM_DEV bool get_seg(const GemmArgs& a, long long lo, long long hi, int i, Seg& s, long long G, long long wk) {
   long long pos = lo;
-  const long long T = a.total, G = gridDim.x;
+  const long long T = a.total;
   for (int j = 0; j <= i; ++j) {
     if (pos >= hi) return false;
     const long long u = pos / a.kb;
@@ -107,7 +113,7 @@ PM_DEV bool get_seg(const GemmArgs& a, long long lo, long long hi, int i, Seg& s
       s.kb1 = (int)(end - u * a.kb);
       const long long first = owner_of(u * a.kb, T, G);
       const long long last = owner_of((u + 1) * a.kb - 1, T, G);
-      s.seg = (int)(blockIdx.x - first);
+      s.seg = (int)(wk - first);
       s.nseg = (int)(last - first + 1);
       return true;
     }
@@ -212,14 +218,15 @@ PM_DEV unsigned long long gtimer() {
       g_gemm_trace[blockIdx.x * 8 + (slot)] = gtimer();                             \
   } while (0)
 
-template <int BN>
+template <int BN, int NH>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, NH>;
+  constexpr bool PAIR = NH == 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sa = smem;
-  uint8_t* sb = smem + C::STAGES * A_BYTES;
+  uint8_t* sa = smem;                                     // [STAGES][NH x 128 rows][64] weights
+  uint8_t* sb = smem + C::STAGES * NH * SUB_BYTES;        // [STAGES][BN rows][64] X tile
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;      // [2]
@@ -229,38 +236,46 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
   int* red_idx = reinterpret_cast<int*>(red_val + 4 * BN);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long lo = range_lo(blockIdx.x, a.total, gridDim.x);
-  const long long hi = range_lo(blockIdx.x + 1, a.total, gridDim.x);
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0;   // which 128-row half (pair mode)
+  const long long G = PAIR ? gridDim.x >> 1 : gridDim.x, wk = PAIR ? blockIdx.x >> 1 : blockIdx.x;
+  const long long lo = range_lo(wk, a.total, G);
+  const long long hi = range_lo(wk + 1, a.total, G);
 
   pdl_trigger();
   PM_TRACE(0);
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmap_x);
-    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    // full: own producer's arrive + tx (own weights, both X halves);
+    // empty: both CTAs' MMA commits (the X multicast writes both CTAs' stage)
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], PAIR ? 2 : 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 4); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();             // partner's barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- producer: one 32 KB bulk weight chunk + one X tile per stage
+      // ---------------- producer: own 16 KB weight half-chunk + half of the X tile (multicast)
       const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+      auto wsrc = [&](int wunit, int kb) {
+        return a.w + (((size_t)wunit * a.kb + kb) * 2 + crank) * SUB_BYTES;   // NH halves from here
+      };
       // Weights do not depend on the previous kernel: stream the first stages
       // of weights before waiting on it (the activation tiles wait).
       int pre = 0;
       {
         Seg sg;
         int it = 0;
-        for (int i = 0; it < C::STAGES && get_seg(a, lo, hi, i, sg); ++i) {
+        for (int i = 0; it < C::STAGES && get_seg(a, lo, hi, i, sg, G, wk); ++i) {
           const int wunit = sg.unit % a.n_units;
           for (int kb = sg.kb0; kb < sg.kb1 && it < C::STAGES; ++kb, ++it) {
             mbar_arrive_expect_tx(&full[it], C::STAGE);
-            bulk_load(sa + it * A_BYTES, a.w + ((size_t)wunit * a.kb + kb) * A_BYTES, A_BYTES, &full[it], pol_w);
+            bulk_load(sa + it * NH * SUB_BYTES, wsrc(wunit, kb), NH * SUB_BYTES, &full[it], pol_w);
           }
         }
         pre = it;
@@ -268,16 +283,21 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
       pdl_wait();
       int it = 0;
       Seg sg;
-      for (int i = 0; get_seg(a, lo, hi, i, sg); ++i) {
+      for (int i = 0; get_seg(a, lo, hi, i, sg, G, wk); ++i) {
         const int wunit = sg.unit % a.n_units, ttile = sg.unit / a.n_units;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
           if (it >= pre) {
+            // both CTAs released the stage (the X multicast overwrites both)
             if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
             mbar_arrive_expect_tx(&full[s], C::STAGE);
-            bulk_load(sa + s * A_BYTES, a.w + ((size_t)wunit * a.kb + kb) * A_BYTES, A_BYTES, &full[s], pol_w);
+            bulk_load(sa + s * NH * SUB_BYTES, wsrc(wunit, kb), NH * SUB_BYTES, &full[s], pol_w);
           }
-          tma_load_2d(sb + s * C::B_BYTES, &tmap_x, &full[s], kb * BK, ttile * BN, pol_x);
+          if (PAIR)
+            tma_load_2d_mc(sb + s * C::B_BYTES + crank * (BN / 2) * 128, &tmap_x, &full[s], kb * BK,
+                           ttile * BN + crank * (BN / 2), (uint16_t)0x3, pol_x);
+          else
+            tma_load_2d(sb + s * C::B_BYTES, &tmap_x, &full[s], kb * BK, ttile * BN, pol_x);
         }
       }
       // Every load of this CTA is issued: queue this CTA's share of the next
@@ -297,11 +317,11 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
   } else if (warp == 1) {
     pdl_wait();
     if (lane == 0) {
-      // ---------------- MMA issuer
+      // ---------------- MMA issuer: D[128 rows of this half][BN tokens]
       constexpr uint32_t idesc = umma_idesc_bf16(128, BN);
       int it = 0;
       Seg sg;
-      for (int i = 0; get_seg(a, lo, hi, i, sg); ++i) {
+      for (int i = 0; get_seg(a, lo, hi, i, sg, G, wk); ++i) {
         const int b = i % C::ACC_BUFS;
         if (i >= C::ACC_BUFS) mbar_wait(&tempty[b], ((i / C::ACC_BUFS) - 1) & 1);
         tc_fence_after();
@@ -311,14 +331,17 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
           tc_fence_after();
           const uint64_t db = umma_desc_sw128(smem_u32(sb + s * C::B_BYTES));
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint64_t da = umma_desc_sw128(smem_u32(sa + s * A_BYTES + h * SUB_BYTES));
-            const uint32_t acc = tmem + (uint32_t)((b * 2 + h) * BN);
+          for (int h = 0; h < NH; ++h) {
+            const uint64_t da = umma_desc_sw128(smem_u32(sa + (s * NH + h) * SUB_BYTES));
+            const uint32_t acc = tmem + (uint32_t)((b * NH + h) * BN);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)
               tc_mma_bf16(acc, da + 2 * kk, db + 2 * kk, idesc, (kb > sg.kb0 || kk > 0) ? 1u : 0u);
           }
-          tc_commit(&empty[s]);
+          if (PAIR)
+            tc_commit_mc(&empty[s], (uint16_t)0x3);   // release the stage in both CTAs
+          else
+            tc_commit(&empty[s]);
         }
         tc_commit(&tfull[b]);
       }
@@ -329,31 +352,36 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
     pdl_wait();
     const int q = warp & 3;
     const int wq = warp - EPI_WARP0;
+    const int rh = (int)crank * 128 + q * 32 + lane;     // row of the 256-row unit
     Seg sg;
-    for (int i = 0; get_seg(a, lo, hi, i, sg); ++i) {
+    for (int i = 0; get_seg(a, lo, hi, i, sg, G, wk); ++i) {
       const int b = i % C::ACC_BUFS;
       mbar_wait(&tfull[b], (i / C::ACC_BUFS) & 1);
       tc_fence_after();
       const int tok_tile = sg.unit / a.n_units, wunit = sg.unit % a.n_units;
       const int tok_base = tok_tile * BN;
       const int tok_end = min(BN, a.m_tok - tok_base);
-      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NH * BN);
       const bool whole = sg.nseg == 1;
       const bool argmax = whole && a.epilogue == EPI_LOGITS_ARGMAX;
       if (!(a.debug & 1)) {
         if (whole) {
-          const int n0 = wunit * UNIT_ROWS + q * 32 + lane;
+          const int n0 = wunit * UNIT_ROWS + rh;
           for (int c0 = 0; c0 < BN && c0 < tok_end; c0 += 16) {
-            float v0[16], v1[16];
-            tmem_ld16(trow + (b * 2 + 0) * BN + c0, v0);
-            tmem_ld16(trow + (b * 2 + 1) * BN + c0, v1);
-            pair_epilogue(a, n0, tok_base, tok_end, c0, v0, v1, lane);
+            float v[NH][16];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) tmem_ld16(trow + h * BN + c0, v[h]);
+            if (NH == 2)
+              pair_epilogue(a, n0, tok_base, tok_end, c0, v[0], v[NH - 1], lane);
+            else
+              row_epilogue<16>(a, n0, tok_base, tok_end, c0, v[0], lane);
             if (argmax) {
+              // the thread's best over its NH rows, then one warp reduction
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
-                float bv = n0 < a.n_out ? v0[j] : -INFINITY;
+                float bv = n0 < a.n_out ? v[0][j] : -INFINITY;
                 int bi = n0;
-                if (n0 + 128 < a.n_out && v1[j] > bv) { bv = v1[j]; bi = n0 + 128; }
+                if (NH == 2 && n0 + 128 < a.n_out && v[NH - 1][j] > bv) { bv = v[NH - 1][j]; bi = n0 + 128; }
                 warp_argmax(bv, bi);
                 if (lane == 0) { red_val[wq * BN + c0 + j] = bv; red_idx[wq * BN + c0 + j] = bi; }
               }
@@ -361,16 +389,15 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
           }
         } else {
           // partial segment: fp32 [seg][col][256 rows] at L2; the post kernel finishes the unit
-          float* dst = a.ws + ((size_t)sg.unit * a.max_segs + sg.seg) * (size_t)BN * UNIT_ROWS;
+          float* dst = a.ws + ((size_t)sg.unit * a.max_segs + sg.seg) * (size_t)BN * UNIT_ROWS + rh;
           for (int c0 = 0; c0 < BN && c0 < tok_end && !(a.debug & 4); c0 += 16) {
-            float v0[16], v1[16];
-            tmem_ld16(trow + (b * 2 + 0) * BN + c0, v0);
-            tmem_ld16(trow + (b * 2 + 1) * BN + c0, v1);
+            float v[NH][16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              __stcg(&dst[(size_t)(c0 + j) * UNIT_ROWS + q * 32 + lane], v0[j]);
-              __stcg(&dst[(size_t)(c0 + j) * UNIT_ROWS + 128 + q * 32 + lane], v1[j]);
-            }
+            for (int h = 0; h < NH; ++h) tmem_ld16(trow + h * BN + c0, v[h]);
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+#pragma unroll
+              for (int j = 0; j < 16; ++j) __stcg(&dst[(size_t)(c0 + j) * UNIT_ROWS + h * 128], v[h][j]);
           }
         }
       }
@@ -380,6 +407,9 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
       if (lane == 0) mbar_arrive(&tempty[b]);
       if (argmax && !(a.debug & 1)) {
         epi_bar();
+        // argmax tiles are 128-row halves: this CTA's rows go to tile 2u + crank
+        // (pair) or, for a whole-unit CTA, the unit's best to tile 2u and an
+        // empty entry to tile 2u + 1
         for (int c = threadIdx.x - EPI_WARP0 * 32; c < tok_end; c += 128) {
           float bv = red_val[c];
           int bi = red_idx[c];
@@ -388,8 +418,12 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
               bv = red_val[w * BN + c];
               bi = red_idx[w * BN + c];
             }
-          a.amax_val[(size_t)wunit * a.m_cap + tok_base + c] = bv;
-          a.amax_idx[(size_t)wunit * a.m_cap + tok_base + c] = bi;
+          a.amax_val[(size_t)(wunit * 2 + crank) * a.m_cap + tok_base + c] = bv;
+          a.amax_idx[(size_t)(wunit * 2 + crank) * a.m_cap + tok_base + c] = bi;
+          if (NH == 2) {
+            a.amax_val[(size_t)(wunit * 2 + 1) * a.m_cap + tok_base + c] = -INFINITY;
+            a.amax_idx[(size_t)(wunit * 2 + 1) * a.m_cap + tok_base + c] = 0x7fffffff;
+          }
         }
         epi_bar();
       }
@@ -397,13 +431,12 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();             // no CTA leaves while its partner may still signal it
   if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
-// Finishes the units the stream-K partition split across CTAs: sums the
-// per-segment fp32 partials in segment order (deterministic) and applies the
-// epilogue.  One CTA per (split unit, RC-column chunk); thread = output row;
-// every segment's loads are in flight at once (segments <= MAX_SEGS).
+// ---------------------------------------------------------------- post kernels
+// One CTA per (unit, RC token columns), thread = row of the 256-row unit.
 #ifndef PM_RC
 #define PM_RC 4
 #endif
@@ -476,13 +509,15 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) 
       if (lane == 0) { sv[warp][j] = bv; si[warp][j] = bi; }
     }
     __syncthreads();
-    if (r < RC && c0 + r < tok_end) {
-      float bv = sv[0][r];
-      int bi = si[0][r];
-      for (int w = 1; w < 8; ++w)
-        if (sv[w][r] > bv || (sv[w][r] == bv && si[w][r] < bi)) { bv = sv[w][r]; bi = si[w][r]; }
-      a.amax_val[(size_t)wunit * a.m_cap + tok_base + c0 + r] = bv;
-      a.amax_idx[(size_t)wunit * a.m_cap + tok_base + c0 + r] = bi;
+    // one argmax tile per 128-row half (warps 0-3 / 4-7), as the GEMM writes them
+    if (r < 2 * RC && c0 + (r % RC) < tok_end) {
+      const int j = r % RC, h = r / RC;
+      float bv = sv[4 * h][j];
+      int bi = si[4 * h][j];
+      for (int w = 4 * h + 1; w < 4 * h + 4; ++w)
+        if (sv[w][j] > bv || (sv[w][j] == bv && si[w][j] < bi)) { bv = sv[w][j]; bi = si[w][j]; }
+      a.amax_val[(size_t)(wunit * 2 + h) * a.m_cap + tok_base + c0 + j] = bv;
+      a.amax_idx[(size_t)(wunit * 2 + h) * a.m_cap + tok_base + c0 + j] = bi;
     }
   }
 }
@@ -694,24 +729,36 @@ __global__ void __launch_bounds__(256) gemm_qkv_rope_kernel(GemmArgs a, int grid
 
 enum Post : int { POST_NONE = 0, POST_RESID_NORM = 1, POST_QKV_ROPE = 2 };
 
-template <int BN>
-int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int post = POST_NONE,
-           const NormArgs* na = nullptr, const RopeArgs* ra = nullptr) {
-  using C = Cfg<BN>;
+template <int BN, int NH>
+int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int post, const NormArgs* na,
+           const RopeArgs* ra) {
+  using C = Cfg<BN, NH>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_stream_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_stream_kernel<BN, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  cudaError_t e = launch_k(gemm_stream_kernel<BN>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, *tx, a);
+  cudaError_t e;
+  if (NH == 1)   // grid = 2 x workers: each stream-K worker is a (2,1,1) cluster
+    e = launch_k_cluster(gemm_stream_kernel<BN, NH>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, 2, *tx, a);
+  else
+    e = launch_k(gemm_stream_kernel<BN, NH>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, *tx, a);
   if (e != cudaSuccess) return (int)e;
+  const int G = NH == 1 ? grid / 2 : grid;
   const dim3 pg(a.n_units * a.tok_tiles, BN / RC);
   if (post == POST_QKV_ROPE)   // every unit (whole ones read the stored bf16)
-    return (int)launch_k(gemm_qkv_rope_kernel<BN>, pg, dim3(256), 0, st, a, grid, *ra);
+    return (int)launch_k(gemm_qkv_rope_kernel<BN>, pg, dim3(256), 0, st, a, G, *ra);
   if (a.max_segs <= 1 || (a.debug & 1)) return 0;
-  if (post == POST_RESID_NORM) return (int)launch_k(gemm_resid_norm_kernel<BN>, pg, dim3(256), 0, st, a, grid, *na);
-  return (int)launch_k(gemm_reduce_kernel<BN>, pg, dim3(256), 0, st, a, grid);
+  if (post == POST_RESID_NORM) return (int)launch_k(gemm_resid_norm_kernel<BN>, pg, dim3(256), 0, st, a, G, *na);
+  return (int)launch_k(gemm_reduce_kernel<BN>, pg, dim3(256), 0, st, a, G);
+}
+
+template <int BN>
+int launch_any(bool pair, const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int post = POST_NONE,
+               const NormArgs* na = nullptr, const RopeArgs* ra = nullptr) {
+  return pair ? launch<BN, 1>(tx, a, grid, st, post, na, ra) : launch<BN, 2>(tx, a, grid, st, post, na, ra);
 }
 
 }  // namespace
@@ -724,16 +771,18 @@ extern "C" int pm_gemm_trace_read(void* dst) {
 // One-time kernel attributes (call before any CUDA-graph capture).
 extern "C" int pm_prepare_gemm(void) {
   cudaError_t e = cudaSuccess;
-#define PM_SET(BN)                                                                                        \
+#define PM_SET(BN, NH)                                                                                    \
   if (e == cudaSuccess)                                                                                   \
-    e = cudaFuncSetAttribute(gemm_stream_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
-  PM_SET(16) PM_SET(32) PM_SET(64) PM_SET(128) PM_SET(256)
+    e = cudaFuncSetAttribute(gemm_stream_kernel<BN, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                             Cfg<BN, NH>::SMEM);
+  PM_SET(16, 1) PM_SET(32, 1) PM_SET(64, 1) PM_SET(128, 1) PM_SET(256, 1)
+  PM_SET(16, 2) PM_SET(32, 2) PM_SET(64, 2) PM_SET(128, 2) PM_SET(256, 2)
 #undef PM_SET
   return (int)e;
 }
 
-// Segments a unit of `kb` k-blocks can be cut into by `grid` CTAs over `total`
-// k-blocks (host helper for workspace sizing; mirrors owner_of()).
+// Segments a unit of `kb` k-blocks can be cut into by `grid` stream-K workers
+// over `total` k-blocks (host helper for workspace sizing; mirrors owner_of()).
 extern "C" int pm_gemm_max_segments(long long total, int kb, int grid) {
   int best = 1;
   for (long long u = 0; u * kb < total; ++u) {
@@ -757,10 +806,11 @@ extern "C" int pm_gemm_split_units(long long total, int kb, int grid) {
   return n;
 }
 
-static int make_args(GemmArgs& a, int& grid, const void* w_packed, int n_out, int n_units, int k, int m_tok,
-                     int bn, int epilogue, void* out, int ld_out, float* ws, int max_segs, float* amax_val,
-                     int* amax_idx, int m_cap, const void* prefetch, unsigned long long prefetch_bytes) {
-  if (k % BK || m_tok < 1 || m_tok > m_cap || grid < 1) return (int)cudaErrorInvalidValue;
+static int make_args(GemmArgs& a, int& grid, int pair, const void* w_packed, int n_out, int n_units, int k,
+                     int m_tok, int bn, int epilogue, void* out, int ld_out, float* ws, int max_segs,
+                     float* amax_val, int* amax_idx, int m_cap, const void* prefetch,
+                     unsigned long long prefetch_bytes) {
+  if (k % BK || m_tok < 1 || m_tok > m_cap || grid < (pair ? 2 : 1)) return (int)cudaErrorInvalidValue;
   const int tok_tiles = (m_tok + bn - 1) / bn;
   a = GemmArgs{reinterpret_cast<const uint8_t*>(w_packed), n_out, n_units, k / BK, m_tok, tok_tiles, epilogue,
                out, ld_out, ws, max_segs, amax_val, amax_idx, m_cap,
@@ -768,7 +818,11 @@ static int make_args(GemmArgs& a, int& grid, const void* w_packed, int n_out, in
                (long long)n_units * tok_tiles * (k / BK), 0};
   if (getenv("PM_GEMM_DEBUG")) a.debug = atoi(getenv("PM_GEMM_DEBUG"));
   if (getenv("PM_GEMM_GRID")) grid = atoi(getenv("PM_GEMM_GRID"));  // tuning experiments only
-  if (grid > a.total) grid = (int)a.total;
+  // grid = CTAs; a worker is one CTA, or a 2-CTA cluster in pair mode; at
+  // most one worker per k-block
+  long long workers = pair ? grid / 2 : grid;
+  if (workers > a.total) workers = a.total;
+  grid = (int)(pair ? 2 * workers : workers);
   return 0;
 }
 
@@ -787,16 +841,16 @@ static int dispatch_bn(int bn, F&& f) {
 // w_packed: [n_units][kb][2][128][64] bf16, each 128x64 tile in the 128B-
 // swizzled K-major UMMA smem image (see ops.pack_weight).
 extern "C" int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
-                       int bn, int grid, int epilogue, void* out, int ld_out, float* ws, int max_segs,
+                       int bn, int grid, int cta_pair, int epilogue, void* out, int ld_out, float* ws, int max_segs,
                        float* amax_val, int* amax_idx, int m_cap, const void* prefetch,
                        unsigned long long prefetch_bytes, void* stream) {
   GemmArgs a;
-  int rc = make_args(a, grid, w_packed, n_out, n_units, k, m_tok, bn, epilogue, out, ld_out, ws, max_segs,
+  int rc = make_args(a, grid, cta_pair, w_packed, n_out, n_units, k, m_tok, bn, epilogue, out, ld_out, ws, max_segs,
                      amax_val, amax_idx, m_cap, prefetch, prefetch_bytes);
   if (rc) return rc;
   auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   auto st = reinterpret_cast<cudaStream_t>(stream);
-  return dispatch_bn(bn, [&](auto c) { return launch<decltype(c)::value>(tx, a, grid, st); });
+  return dispatch_bn(bn, [&](auto c) { return launch_any<decltype(c)::value>(cta_pair, tx, a, grid, st); });
 }
 
 // Residual projection fused with the next RMSNorm: resid[m][0..n_out) +=
@@ -804,20 +858,20 @@ extern "C" int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int 
 // row.  row_counters: int[m_cap], zero at rest (left zero).  When the
 // stream-K partition splits no unit the norm runs as a separate kernel.
 extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k,
-                                     int m_tok, int bn, int grid, float* resid, float* ws, int max_segs, int m_cap,
+                                     int m_tok, int bn, int grid, int cta_pair, float* resid, float* ws, int max_segs, int m_cap,
                                      const void* prefetch, unsigned long long prefetch_bytes, const void* norm_w,
                                      void* xn, float eps, int* row_counters, void* stream) {
   GemmArgs a;
-  int rc = make_args(a, grid, w_packed, n_out, n_units, k, m_tok, bn, EPI_RESID_ADD_F32, resid, n_out, ws,
+  int rc = make_args(a, grid, cta_pair, w_packed, n_out, n_units, k, m_tok, bn, EPI_RESID_ADD_F32, resid, n_out, ws,
                      max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes);
   if (rc) return rc;
   if (n_out % 8 || n_out > 256 * 4 * NORM_V4) return (int)cudaErrorInvalidValue;
   NormArgs na{reinterpret_cast<const bf16*>(norm_w), reinterpret_cast<bf16*>(xn), row_counters,
-              pm_gemm_split_units(a.total, a.kb, grid), eps};
+              pm_gemm_split_units(a.total, a.kb, cta_pair ? grid / 2 : grid), eps};
   auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   auto st = reinterpret_cast<cudaStream_t>(stream);
   const int post = (na.n_split > 0 && !(a.debug & 1)) ? POST_RESID_NORM : POST_NONE;
-  rc = dispatch_bn(bn, [&](auto c) { return launch<decltype(c)::value>(tx, a, grid, st, post, &na); });
+  rc = dispatch_bn(bn, [&](auto c) { return launch_any<decltype(c)::value>(cta_pair, tx, a, grid, st, post, &na); });
   if (rc || post == POST_RESID_NORM) return rc;
   return launch_rmsnorm(resid, norm_w, xn, m_tok, n_out, eps, st);
 }
@@ -827,13 +881,13 @@ extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, i
 // (same contract as pm_qkv_rope_append).  qkv_out [m_cap][n_out] bf16 is
 // scratch for units the partition leaves whole.
 extern "C" int pm_gemm_qkv_rope(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
-                                int bn, int grid, void* qkv_out, float* ws, int max_segs, int m_cap,
+                                int bn, int grid, int cta_pair, void* qkv_out, float* ws, int max_segs, int m_cap,
                                 const void* prefetch, unsigned long long prefetch_bytes, void* q_out, void* pool,
                                 const int* block_table, const int* positions, const float* rope, const void* qn_w,
                                 const void* kn_w, int H, int Hkv, int hd, int layer, int L_s, int max_blocks,
                                 float eps, void* stream) {
   GemmArgs a;
-  int rc = make_args(a, grid, w_packed, n_out, n_units, k, m_tok, bn, EPI_STORE_BF16, qkv_out, n_out, ws,
+  int rc = make_args(a, grid, cta_pair, w_packed, n_out, n_units, k, m_tok, bn, EPI_STORE_BF16, qkv_out, n_out, ws,
                      max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes);
   if (rc) return rc;
   if (n_out != (H + 2 * Hkv) * hd || (hd != 64 && hd != 128) || UNIT_ROWS % hd) return (int)cudaErrorInvalidValue;
@@ -842,5 +896,7 @@ extern "C" int pm_gemm_qkv_rope(const void* w_packed, const void* tmap_x, int n_
               max_blocks, eps};
   auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   auto st = reinterpret_cast<cudaStream_t>(stream);
-  return dispatch_bn(bn, [&](auto c) { return launch<decltype(c)::value>(tx, a, grid, st, POST_QKV_ROPE, nullptr, &ra); });
+  return dispatch_bn(bn, [&](auto c) {
+    return launch_any<decltype(c)::value>(cta_pair, tx, a, grid, st, POST_QKV_ROPE, nullptr, &ra);
+  });
 }

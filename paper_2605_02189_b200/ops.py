@@ -107,19 +107,29 @@ def pack_weight(w: torch.Tensor):
     return out, n_pad // UNIT_ROWS
 
 
+PAIR_MAX_UNITS = 64   # narrower projections run on 2-CTA clusters (measured: QKV/O/down win, gate/up loses)
+
+
 def gemm_plan(n_units: int, kb: int, m_tok: int, sms: int = SMS):
-    """Stream-K geometry of one launch: (bn, grid, max segments per unit).
-    The k-block ranges depend on (units, K, #SMs) only -- not on m_tok for
-    m_tok <= 256 -- which keeps results batch-invariant."""
+    """Stream-K geometry of one launch: (bn, grid CTAs, max segments per
+    unit, token tiles, pair).  Narrow projections (fewer than
+    PAIR_MAX_UNITS 256-row units) use 2-CTA cluster workers -- each CTA
+    computes one 128-row half and the pair shares one multicast activation
+    tile, which halves every split segment's partial and the number of
+    segments; wide ones use one CTA per worker.  The k-block ranges depend on
+    (units, K, #SMs) only -- not on m_tok for m_tok <= 256 -- which keeps
+    results batch-invariant."""
     bn = bn_for(m_tok)
     tt = -(-m_tok // bn)
     total = n_units * tt * kb
-    grid = min(sms, total)
+    pair = n_units < PAIR_MAX_UNITS
+    per = 2 if pair else 1
+    workers = min(sms // per, total)
     import os
     if os.environ.get("PM_GEMM_GRID"):  # tuning experiments only (must match the library's override)
-        grid = min(int(os.environ["PM_GEMM_GRID"]), total)
-    segs = _C.lib().pm_gemm_max_segments(total, kb, grid)
-    return bn, grid, segs, tt
+        workers = min(int(os.environ["PM_GEMM_GRID"]) // per, total)
+    segs = _C.lib().pm_gemm_max_segments(total, kb, workers)
+    return bn, per * workers, segs, tt, pair
 
 
 class GemmWorkspace:
@@ -129,8 +139,9 @@ class GemmWorkspace:
     def __init__(self, m_cap: int, ws_floats: int, max_units: int, vocab_units: int, device):
         self.m_cap = m_cap
         self.ws = torch.empty(max(1, ws_floats), dtype=torch.float32, device=device)
-        self.amax_val = torch.empty(max(1, vocab_units) * m_cap, dtype=torch.float32, device=device)
-        self.amax_idx = torch.empty(max(1, vocab_units) * m_cap, dtype=torch.int32, device=device)
+        # one argmax tile per 128-row half of a vocabulary unit
+        self.amax_val = torch.empty(2 * max(1, vocab_units) * m_cap, dtype=torch.float32, device=device)
+        self.amax_idx = torch.empty(2 * max(1, vocab_units) * m_cap, dtype=torch.int32, device=device)
         # per-row arrival counts of the fused residual + RMSNorm epilogue; kernels leave them zero
         self.row_cnt = torch.zeros(m_cap, dtype=torch.int32, device=device)
 
@@ -139,7 +150,7 @@ class GemmWorkspace:
         need = 1
         for lin in linears:
             for m in sorted({min(m_cap, x) for x in (16, 32, 64, 128, 256, m_cap)}):
-                bn, grid, segs, tt = gemm_plan(lin.n_units, lin.kb, m)
+                bn, grid, segs, tt, _pair = gemm_plan(lin.n_units, lin.kb, m)
                 need = max(need, lin.n_units * tt * segs * bn * UNIT_ROWS)
         return need
 
@@ -180,12 +191,12 @@ class Linear:
                  stream=None, prefetch=None):
         """``prefetch``: optional (tensor, nbytes) the next operation reads
         first; the kernel pulls it into L2 while it drains."""
-        bn, grid, segs, tt = self.plan(m_tok)
+        bn, grid, segs, tt, pair = self.plan(m_tok)
         pf_ptr, pf_bytes = self._pf(prefetch)
 
         def go():
-            _C.call("pm_gemm", _ptr(self.packed), x_maps[bn].ptr, self.n_out, self.n_units, self.k, m_tok, bn,
-                    grid, epilogue, _ptr(out), ld_out, _ptr(ws.ws), segs,
+            _C.call("pm_gemm", _ptr(self.packed), x_maps[bn // 2 if pair else bn].ptr, self.n_out, self.n_units, self.k, m_tok, bn,
+                    grid, int(pair), epilogue, _ptr(out), ld_out, _ptr(ws.ws), segs,
                     _ptr(ws.amax_val), _ptr(ws.amax_idx), ws.m_cap, pf_ptr, pf_bytes, _stream(stream))
         out_b = {EPI_STORE_BF16: 2, EPI_RESID_ADD: 8, EPI_SILU_MUL: 1,
                  EPI_LOGITS_ARGMAX: 4 if out is not None else 0}[epilogue]
@@ -195,12 +206,12 @@ class Linear:
                       stream=None, prefetch=None):
         """resid += x W^T, then xn = RMSNorm(resid) * norm_w -- the residual
         projection fused with the next layer norm (pm_gemm_resid_rmsnorm)."""
-        bn, grid, segs, tt = self.plan(m_tok)
+        bn, grid, segs, tt, pair = self.plan(m_tok)
         pf_ptr, pf_bytes = self._pf(prefetch)
 
         def go():
-            _C.call("pm_gemm_resid_rmsnorm", _ptr(self.packed), x_maps[bn].ptr, self.n_out, self.n_units, self.k,
-                    m_tok, bn, grid, _ptr(resid), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, _ptr(norm_w),
+            _C.call("pm_gemm_resid_rmsnorm", _ptr(self.packed), x_maps[bn // 2 if pair else bn].ptr, self.n_out, self.n_units, self.k,
+                    m_tok, bn, grid, int(pair), _ptr(resid), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, _ptr(norm_w),
                     _ptr(xn), float(eps), _ptr(ws.row_cnt), _stream(stream))
         self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * (8 + 4 + 2), stream, go)
 
@@ -208,20 +219,22 @@ class Linear:
                  rope, qn_w, kn_w, H, Hkv, hd, layer, L_s, eps, stream=None, prefetch=None):
         """QKV projection fused with q/k RMSNorm + RoPE + paged KV append
         (pm_gemm_qkv_rope); ``qkv`` is scratch for units left whole."""
-        bn, grid, segs, tt = self.plan(m_tok)
+        bn, grid, segs, tt, pair = self.plan(m_tok)
         pf_ptr, pf_bytes = self._pf(prefetch)
 
         def go():
-            _C.call("pm_gemm_qkv_rope", _ptr(self.packed), x_maps[bn].ptr, self.n_out, self.n_units, self.k,
-                    m_tok, bn, grid, _ptr(qkv), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, _ptr(q_out),
+            _C.call("pm_gemm_qkv_rope", _ptr(self.packed), x_maps[bn // 2 if pair else bn].ptr, self.n_out, self.n_units, self.k,
+                    m_tok, bn, grid, int(pair), _ptr(qkv), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, _ptr(q_out),
                     _ptr(pool), _ptr(block_table), _ptr(positions), _ptr(rope), _ptr(qn_w), _ptr(kn_w), H, Hkv,
                     hd, layer, L_s, block_table.shape[1], float(eps), _stream(stream))
         self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * 2, stream, go)
 
 
 def activation_maps(buf: torch.Tensor) -> dict:
-    """TMA maps of an activation buffer [m_cap, K] for every supported BN."""
-    return {bn: matrix_tmap(buf, bn) for bn in (16, 32, 64, 128, 256)}
+    """TMA maps of an activation buffer [m_cap, K] with a [rows x 64] box for
+    every token tile BN and half tile BN / 2 (each CTA of a GEMM pair loads
+    half the tile and multicasts it)."""
+    return {rows: matrix_tmap(buf, rows) for rows in (8, 16, 32, 64, 128, 256)}
 
 
 def embed(tok_table, slots, table, resid, M, stream=None):
@@ -326,5 +339,7 @@ def paged_attention(tmap_kv, q, block_table, seq_lens, out, ws: AttnWorkspace, M
 
 
 def argmax_reduce(ws: GemmWorkspace, n_units, M, out_ids, tok_table=None, slots=None, stream=None):
-    _C.call("pm_argmax_reduce", _ptr(ws.amax_val), _ptr(ws.amax_idx), n_units, M, ws.m_cap, _ptr(out_ids),
+    """Greedy ids from the lm_head GEMM's per-tile partials (``n_units`` =
+    the lm_head's 256-row units; two 128-row argmax tiles each)."""
+    _C.call("pm_argmax_reduce", _ptr(ws.amax_val), _ptr(ws.amax_idx), 2 * n_units, M, ws.m_cap, _ptr(out_ids),
             _ptr(tok_table), _ptr(slots), _stream(stream))

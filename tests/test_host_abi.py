@@ -43,11 +43,11 @@ def _owner(idx, T, G):
     return ((idx + 1) * G + T - 1) // T - 1
 
 
-@pytest.mark.parametrize("units,kb,grid", [(24, 64, 148), (16, 64, 148), (594, 64, 148), (2, 4, 8), (1, 1, 1),
+@pytest.mark.parametrize("units,kb,grid", [(24, 64, 148), (16, 64, 148), (594, 64, 148), (2, 4, 8), (1, 1, 2),
                                            (96, 64, 148), (20, 400, 148)])
 def test_stream_k_partition(units, kb, grid):
     T = units * kb
-    G = min(grid, T)
+    G = min(grid // 2, T)   # stream-K workers are CTA pairs
     seen = [0] * T
     for c in range(G):
         lo, hi = c * T // G, (c + 1) * T // G

@@ -50,8 +50,6 @@ for name, (n, k, epi) in shapes.items():
             b.record(st)
         torch.cuda.synchronize()
         best = min(best, a.elapsed_time(b) * 1e-3 / R)
-    if not os.environ.get("PM_GEMM_DEBUG"):
-        assert (ws.counters == 0).all(), "fixup counters not re-armed"
     print(f"{name:8s} [{n}x{k}] M={M} R={R}: {best*1e6:7.1f} us/launch  {n*k*2/best/1e9:6.0f} GB/s  "
           f"ideal@6.65TB/s {n*k*2/6.65e12*1e6:6.1f} us  plan={lins[0].plan(M)}")
     del lins, g
