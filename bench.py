@@ -332,8 +332,15 @@ def run_ours(args):
         kinds = sorted(summ.items(), key=lambda kv_: -kv_[1]["seconds"])
         top, d = kinds[0]
         achieved = (d["bytes"] / d["launches"]) / (d["seconds"] / d["launches"]) / 1e9
+        traffic = None   # DRAM bytes per launch of this kind from the committed ncu capture
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_latest.json")))
+            traffic = tr.get("gemm_call" if top == "gemm" else top, {}).get("dram_bytes_per_launch")
+        except Exception:
+            pass
         out["roofline"] = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peaks["hbm_gbs"],
-                           "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                           "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                           "algorithmic_bytes_per_launch": d["bytes"] / d["launches"],
                            "peak_source": peaks_src, "share_of_step": d["seconds"] / prof_s,
                            "per_kind": {k: {"launches": v["launches"], "GBps": v["bytes"] / v["seconds"] / 1e9,
                                             "share": v["seconds"] / prof_s} for k, v in summ.items()},
