@@ -254,8 +254,10 @@ class DecodeEngine:
         self.n_evicted += len(work.evicted) + len(work.relief_evicted)
         self.n_prefetched += len(work.prefetch)
         recs = []
+        info = {"plan": work.plan, "batch_tokens": work.batch_tokens, "completed": list(work.completed),
+                "resident_tokens": self.control.resident_tokens, "capacity_tokens": self.control.capacity_tokens}
         for ex, kv in self.stages:
-            rec = {"t": t, "M": M}
+            rec = {"t": t, "M": M, "info": info}
             kv.prefetch(t, work, rec)
             recs.append(rec)
         self._upload_meta(work.rows, work.positions, work.tables)
@@ -281,6 +283,48 @@ class DecodeEngine:
             n += 1
         torch.cuda.synchronize()
         return n
+
+    def emit_trace(self, origin, trace: EventTrace = None) -> EventTrace:
+        """Decode events of every step so far in the reference's trace schema
+        (REF pipeline_sim.py:410-421, 460-482, 505-510, 221-233), timed by the
+        CUDA events the KV engines recorded, in seconds since ``origin``."""
+        tr = trace if trace is not None else self.trace
+        torch.cuda.synchronize()
+
+        def ts(ev):
+            return origin.elapsed_time(ev) * 1e-3
+
+        for si, (ex, kv) in enumerate(self.stages):
+            h2d_name, d2h_name = f"h2d{si}", f"d2h{si}"
+            for rec in kv.records:
+                if "start" not in rec or "end" not in rec:
+                    continue
+                info, p = rec.get("info", {}), rec.get("info", {}).get("plan")
+                it, b = rec["t"], (p.exec_batch_index if p is not None else None)
+                t0, t1 = ts(rec["start"]), ts(rec["end"])
+                if "ready" in rec and t0 - ts(rec["ready"]) > 1e-6:
+                    tr.emit(ts(rec["ready"]), "stall_start", iter=it, batch=b, stage=si, reason="prefetch_wait")
+                    tr.emit(t0, "stall_end", iter=it, batch=b, stage=si, reason="prefetch_wait")
+                payload = dict(phase="decode", stage=si, iter=it, batch=b)
+                if si == 0 and p is not None:
+                    payload.update(exec_seconds=t1 - t0, predicted_seconds=p.predicted_exec_seconds,
+                                   batch_tokens=info["batch_tokens"], resident_tokens_total=info["resident_tokens"],
+                                   next_residual_tokens=p.residual_tokens, next_prefetched_tokens=p.prefetch_tokens,
+                                   budget_tokens=p.prefetch_budget_tokens, capacity_tokens=info["capacity_tokens"],
+                                   steady=p.steady)
+                tr.emit(t0, "stage_compute_start", **payload)
+                tr.emit(t1, "stage_compute_end", phase="decode", stage=si, iter=it, batch=b)
+                for kind, ch, direction, tag in (("h2d", h2d_name, "h2d", "kv_prefetch"),
+                                                 ("d2h", d2h_name, "d2h", "kv_offload_decode")):
+                    if f"{kind}_start" in rec:
+                        pl = dict(channel=ch, direction=direction, priority="low", bytes=rec.get(f"{kind}_bytes", 0),
+                                  tag=[tag, it])
+                        tr.emit(ts(rec[f"{kind}_start"]), "transfer_start", **pl)
+                        tr.emit(ts(rec[f"{kind}_end"]), "transfer_end", **pl)
+                if si == len(self.stages) - 1:
+                    for rid in info.get("completed", []):
+                        tr.emit(t1, "request_complete", request=int(rid), iter=it)
+        return tr
 
     def finalize_metrics(self, wall_seconds: float):
         m = self.metrics
@@ -312,5 +356,6 @@ def run_decode(state: SchedulerState, cfg: ClusterConfig, params: EstimatorParam
     torch.cuda.synchronize()
     wall = start.elapsed_time(end) * 1e-3
     m = eng.finalize_metrics(wall)
+    eng.emit_trace(start)
     eng.trace.finalize()
     return eng.trace, m
