@@ -214,8 +214,7 @@ PM_DEV unsigned long long gtimer() {
 }
 #define PM_TRACE(slot)                                                              \
   do {                                                                              \
-    if ((a.debug & 8) && threadIdx.x == EPI_WARP0 * 32 && blockIdx.x < 148)        \
-      g_gemm_trace[blockIdx.x * 8 + (slot)] = gtimer();                             \
+    if ((a.debug & 8) && blockIdx.x < 148) g_gemm_trace[blockIdx.x * 8 + (slot)] = gtimer(); \
   } while (0)
 
 template <int BN, int NH>
@@ -242,7 +241,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
   const long long hi = range_lo(wk + 1, a.total, G);
 
   pdl_trigger();
-  PM_TRACE(0);
+  if (threadIdx.x == 0) PM_TRACE(0);
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmap_x);
     // full: own producer's arrive + tx (own weights, both X halves);
@@ -281,6 +280,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
         pre = it;
       }
       pdl_wait();
+      PM_TRACE(1);   // producer past the dependency wait
       int it = 0;
       Seg sg;
       for (int i = 0; get_seg(a, lo, hi, i, sg, G, wk); ++i) {
@@ -345,6 +345,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
         }
         tc_commit(&tfull[b]);
       }
+      PM_TRACE(2);   // last MMA issued
     }
     __syncwarp();
   } else {
@@ -429,6 +430,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
       }
     }
   }
+  if (threadIdx.x == EPI_WARP0 * 32) PM_TRACE(3);   // epilogue done
   tc_fence_before();
   __syncthreads();
   if (PAIR) cluster_sync();             // no CTA leaves while its partner may still signal it
@@ -437,10 +439,8 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
 
 // ---------------------------------------------------------------- post kernels
 // One CTA per (unit, RC token columns), thread = row of the 256-row unit.
-#ifndef PM_RC
-#define PM_RC 4
-#endif
-constexpr int RC = PM_RC, MAX_SEGS = 8;
+// RC is chosen per launch so the grid fits in about one wave (launch()).
+constexpr int MAX_SEGS = 8;
 
 // segment count of stream-K unit `unit` (mirrors get_seg / pm_gemm_max_segments)
 PM_DEV int unit_segments(const GemmArgs& a, int unit, int grid) {
@@ -453,7 +453,7 @@ PM_DEV int unit_segments(const GemmArgs& a, int unit, int grid) {
 // v[j] = sum over the unit's segments (in segment order) of row r, column c0+j.
 // Rounds of MAX_SEGS segments; each round issues all its loads before the
 // first add (volatile keeps them in flight).
-template <int BN>
+template <int BN, int RC>
 PM_DEV void sum_partials(const GemmArgs& a, int unit, int nseg, int c0, int r, float (&v)[RC]) {
   const float* part = a.ws + (size_t)unit * a.max_segs * BN * UNIT_ROWS + (size_t)c0 * UNIT_ROWS + r;
 #pragma unroll
@@ -482,7 +482,7 @@ PM_DEV void sum_partials(const GemmArgs& a, int unit, int nseg, int c0, int r, f
 
 // Finishes the units the stream-K partition split across CTAs and applies
 // the epilogue.  One CTA per (split unit, RC-column chunk); thread = row.
-template <int BN>
+template <int BN, int RC>
 __global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) {
   pdl_trigger();
   pdl_wait();
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) 
   const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
   const int n = wunit * UNIT_ROWS + r;
   float v[RC];
-  sum_partials<BN>(a, unit, nseg, c0, r, v);
+  sum_partials<BN, RC>(a, unit, nseg, c0, r, v);
   row_epilogue<RC>(a, n, tok_base, tok_end, c0, v, lane);
   if (a.epilogue == EPI_LOGITS_ARGMAX) {
     __shared__ float sv[8][RC];
@@ -576,7 +576,7 @@ PM_DEV void block_rmsnorm_rows(const float* x, int ld, const int* rows, int nrow
   }
 }
 
-template <int BN>
+template <int BN, int RC>
 __global__ void __launch_bounds__(256) gemm_resid_norm_kernel(GemmArgs a, int grid, NormArgs na) {
   pdl_trigger();
   pdl_wait();
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(256) gemm_resid_norm_kernel(GemmArgs a, int gr
   const int r = threadIdx.x;
   const int n = wunit * UNIT_ROWS + r;
   float v[RC];
-  sum_partials<BN>(a, unit, nseg, c0, r, v);
+  sum_partials<BN, RC>(a, unit, nseg, c0, r, v);
   float* o = reinterpret_cast<float*>(a.out);
   if (n < a.n_out) {
     float res[RC];   // every residual load in flight before the first store
@@ -635,7 +635,7 @@ struct RopeArgs {
   float eps;
 };
 
-template <int BN>
+template <int BN, int RC>
 __global__ void __launch_bounds__(256) gemm_qkv_rope_kernel(GemmArgs a, int grid, RopeArgs ra) {
   pdl_trigger();
   const int unit = blockIdx.x, c0 = blockIdx.y * RC;
@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(256) gemm_qkv_rope_kernel(GemmArgs a, int grid
   pdl_wait();
   float v[RC];
   if (nseg > 1) {
-    sum_partials<BN>(a, unit, nseg, c0, r, v);
+    sum_partials<BN, RC>(a, unit, nseg, c0, r, v);
 #pragma unroll
     for (int j = 0; j < RC; ++j) v[j] = __bfloat162float(__float2bfloat16(v[j]));
   } else {
@@ -747,12 +747,25 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int pos
     e = launch_k(gemm_stream_kernel<BN, NH>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, *tx, a);
   if (e != cudaSuccess) return (int)e;
   const int G = NH == 1 ? grid / 2 : grid;
-  const dim3 pg(a.n_units * a.tok_tiles, BN / RC);
-  if (post == POST_QKV_ROPE)   // every unit (whole ones read the stored bf16)
-    return (int)launch_k(gemm_qkv_rope_kernel<BN>, pg, dim3(256), 0, st, a, G, *ra);
-  if (a.max_segs <= 1 || (a.debug & 1)) return 0;
-  if (post == POST_RESID_NORM) return (int)launch_k(gemm_resid_norm_kernel<BN>, pg, dim3(256), 0, st, a, G, *na);
-  return (int)launch_k(gemm_reduce_kernel<BN>, pg, dim3(256), 0, st, a, G);
+  if (post == POST_NONE && (a.max_segs <= 1 || (a.debug & 1))) return 0;
+  if (post == POST_RESID_NORM && (a.max_segs <= 1 || (a.debug & 1))) return 0;
+  // columns per post CTA (4: measured best for the decode shapes)
+  const long long units = (long long)a.n_units * a.tok_tiles;
+  static int rc_env = -1;   // tuning override PM_POST_RC (2, 4, 8 or 16)
+  if (rc_env < 0) rc_env = getenv("PM_POST_RC") ? atoi(getenv("PM_POST_RC")) : 4;
+  const int rc = rc_env;
+  auto go = [&](auto rcc) -> int {
+    constexpr int R = decltype(rcc)::value;
+    const dim3 pg((unsigned)units, BN / R);
+    if (post == POST_QKV_ROPE)   // every unit (whole ones read the stored bf16)
+      return (int)launch_k(gemm_qkv_rope_kernel<BN, R>, pg, dim3(256), 0, st, a, G, *ra);
+    if (post == POST_RESID_NORM) return (int)launch_k(gemm_resid_norm_kernel<BN, R>, pg, dim3(256), 0, st, a, G, *na);
+    return (int)launch_k(gemm_reduce_kernel<BN, R>, pg, dim3(256), 0, st, a, G);
+  };
+  if (rc == 2) return go(std::integral_constant<int, 2>{});
+  if (rc == 8 && BN >= 8) return go(std::integral_constant<int, 8>{});
+  if (rc == 16 && BN >= 16) return go(std::integral_constant<int, 16>{});
+  return go(std::integral_constant<int, 4>{});
 }
 
 template <int BN>

@@ -33,8 +33,9 @@ t = buf.reshape(148, 8).astype(np.int64)
 t0 = t[:, 0].min()
 rel = np.where(t > 0, t - t0, -1)
 print(f"shape {n}x{k} M={M} plan={lins[0].plan(M)}")
-print("cta  start  loopend  w1done stage1 fix1   w2done stage2 fix2   (us)")
+print("cta   start  waited lastmma  epi_end (us)")
 for c in list(range(0, 148, 9)) + [147]:
-    print(f"{c:3d} " + " ".join(f"{v/1e3:6.1f}" if v >= 0 else "     -" for v in rel[c, :8]))
-print(f"max loop end {rel[:,1].max()/1e3:.1f} us, min loop end {rel[:,1].min()/1e3:.1f}, "
-      f"max fix end {max(rel[:,4].max(), rel[:,7].max())/1e3:.1f} us")
+    print(f"{c:3d} " + " ".join(f"{v/1e3:7.1f}" if v >= 0 else "      -" for v in rel[c, :4]))
+for k, name in [(1, "waited"), (2, "last mma"), (3, "epilogue end")]:
+    v = rel[:, k][rel[:, k] >= 0]
+    print(f"{name:13s} min {v.min()/1e3:7.1f} median {np.median(v)/1e3:7.1f} max {v.max()/1e3:7.1f}")

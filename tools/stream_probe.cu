@@ -53,8 +53,9 @@ __global__ void __launch_bounds__(64, 1) probe(const __grid_constant__ CUtensorM
   __syncthreads();
 }
 
-int main() {
+int main(int argc, char** argv) {
   const size_t bytes = 2ull << 30;  // 2 GiB
+  const int grid = argc > 1 ? atoi(argv[1]) : 148;  // CTAs (one per SM)
   uint8_t* buf;
   cudaMalloc(&buf, bytes);
   cudaMemset(buf, 1, bytes);
@@ -70,7 +71,7 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int mode = 0; mode < 2; ++mode) {
+  for (int mode = 0; mode < 1; ++mode) {
     for (int cb : {16384, 32768, 65536}) {
       for (int stages : {2, 3, 4, 6, 8, 12}) {
         if ((size_t)cb * stages > 200 * 1024) continue;
@@ -81,16 +82,17 @@ int main() {
         float best = 1e9;
         for (int it = 0; it < 5; ++it) {
           cudaEventRecord(a);
-          k<<<148, 64, smem>>>(tm, buf, chunks, cb, stages);
+          k<<<grid, 64, smem>>>(tm, buf, chunks, cb, stages);
           cudaEventRecord(b);
           cudaEventSynchronize(b);
           float ms;
           cudaEventElapsedTime(&ms, a, b);
           if (ms < best) best = ms;
         }
-        long long moved = (chunks / 148) * 148 * (long long)cb;
-        printf("%s chunk=%6d stages=%2d  %7.0f GB/s  (%s)\n", mode == 0 ? "bulk1d" : "tma2d ", cb, stages,
-               moved / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+        long long moved = (chunks / grid) * grid * (long long)cb;
+        printf("grid=%3d %s chunk=%6d stages=%2d  %7.0f GB/s  %6.1f GB/s/SM (%s)\n", grid,
+               mode == 0 ? "bulk1d" : "tma2d ", cb, stages, moved / (best * 1e-3) / 1e9,
+               moved / (best * 1e-3) / 1e9 / grid, cudaGetErrorString(cudaGetLastError()));
       }
     }
   }
