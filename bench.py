@@ -195,13 +195,13 @@ def run_ours(args):
     kv_tok_sum = 0
     start_ev, end_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
-        start_ev.record(kv.compute)
+        eng.begin_region(start_ev)
         for i in range(args.steps):
             work = eng.step()
             assert work is not None, "workload ended inside the timed region"
             tokens += len(work.rows)
             kv_tok_sum += sum(work.positions) + len(work.rows)
-        end_ev.record(kv.compute)
+        eng.end_region(end_ev)
         torch.cuda.synchronize()
     dev_s = start_ev.elapsed_time(end_ev) * 1e-3
     h2d_b, d2h_b = kv.h2d_bytes - h2d0, kv.d2h_bytes - d2h0
@@ -214,16 +214,27 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_tok, meta_b, e2e_h2d0, e2e_d2h0 = 0, 0, kv.h2d_bytes, kv.d2h_bytes
     w0 = time.perf_counter()
+    pending = None   # (event, ...) of the previous step's ids readback
     for i in range(args.steps):
+        t = eng.t
         work = eng.step()
         assert work is not None, "workload ended inside the e2e region"
         M = len(work.rows)
         e2e_tok += M
         meta_b += (eng.bucket(M) * (eng.max_blocks + 3) + 2 + 2 * M * eng.stages[0][0].aws.max_chunks) * 4
-        last_ex, last_kv = eng.stages[-1]
-        with torch.cuda.stream(last_kv.compute):
-            ids_host[i, :M].copy_(last_ex.out_ids[:M], non_blocking=True)
-        last_kv.compute.synchronize()
+        # the step's greedy ids -> pinned host memory on its own stream; the
+        # host waits for step t-1's ids while step t runs (one micro-batch of
+        # slack, as a serving loop with two micro-batches in flight does)
+        lane_stream = eng.stages[-1][1].streams[eng.lane_of(t)]
+        with torch.cuda.stream(lane_stream):
+            ids_host[i, :M].copy_(eng.last_executor(t).out_ids[:M], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(lane_stream)
+        if pending is not None:
+            pending.synchronize()
+        pending = ev
+    if pending is not None:
+        pending.synchronize()
     wall = time.perf_counter() - w0
     e2e_h2d, e2e_d2h = kv.h2d_bytes - e2e_h2d0, kv.d2h_bytes - e2e_d2h0
     if dist:
@@ -272,7 +283,8 @@ def run_ours(args):
                 "d2h_bytes_per_step": int((e2e_d2h + e2e_tok * 4) / args.steps),
                 "note": "K further steps through the public engine API (DecodeEngine.step, the simulate_decode "
                         "loop), wall clock, each step's greedy ids copied to pinned host memory and waited for "
-                        "before the next step; H2D = KV prefetch + step metadata, D2H = KV offload + ids"},
+                        "by the host one step later (two micro-batches in flight); H2D = KV prefetch + step "
+                        "metadata, D2H = KV offload + ids"},
         "kv_transfer_hidden_fraction": hidden,
         "kv_transfer": {"h2d_bytes": h2d_b, "d2h_bytes": d2h_b, "h2d_busy_s": h2d_busy,
                         "d2h_busy_s": d2h_busy, "exposed_stall_s": stall,
@@ -290,16 +302,18 @@ def run_ours(args):
         # around every GEMM / attention launch on the compute stream
         timer = ops.KernelTimer()
         ops.TIMER = timer
+        eng.serialize_lanes = True   # per-launch events must not see the other lane's kernels
         a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a_ev.record(kv.compute)
+        eng.begin_region(a_ev)
         n_prof = 0
         for i in range(args.steps):
             if eng.step() is None:
                 break
             n_prof += 1
-        b_ev.record(kv.compute)
+        eng.end_region(b_ev)
         torch.cuda.synchronize()
         ops.TIMER = None
+        eng.serialize_lanes = False
         prof_s = a_ev.elapsed_time(b_ev) * 1e-3
         summ = timer.summary()
         kinds = sorted(summ.items(), key=lambda kv_: -kv_[1]["seconds"])

@@ -81,7 +81,7 @@ class DecodeEngine:
                  requests: dict, *, pp: int = 1, device="cuda", mode="dynamic", quota_tokens=0,
                  seed: int = 0, m_cap: int = None, timing=True, kv_init="random", prompts=None,
                  record_logits=False, max_pos=None, trace: EventTrace = None, graphs: bool = True,
-                 local_stages=None, staging_pool_requests: int = 2):
+                 local_stages=None, staging_pool_requests: int = 2, lanes: int = None):
         """``local_stages``: which of the ``pp`` stages this process hosts
         (default all; one rank per stage under torchrun, see pipeline.py)."""
         self.spec, self.cfg, self.params = spec, cfg, params
@@ -121,15 +121,30 @@ class DecodeEngine:
         self.bpc = self.stages[0][0].aws.bpc
         self.attn_hkv, self.attn_workers = self.stages[0][0].aws.Hkv, self.stages[0][0].aws.workers
         self.meta = _MetaRing(self.m_cap, self.max_blocks, extra=self.work_len)
+        # lanes = micro-batches in flight on one GPU: consecutive rotation steps
+        # (different micro-batches, independent compute) run on their own
+        # compute streams with their own activation buffers and graphs, so one
+        # step's latency-bound kernels overlap the other's weight streaming.
+        # Ordering through the KV pool stays event-based per step (KvEngine).
+        if lanes is None:
+            lanes = 2 if (pp == 1 and local_stages is None) else 1
+        self.serialize_lanes = False   # True: step t waits for step t-1 (per-kernel timing passes)
+        self.lanes = lanes
+        self.lane_stages = [self.stages]
+        for li in range(1, lanes):
+            self.lane_stages.append([(ex.clone_lane(), kv) for ex, kv in self.stages])
+            for _, kv in self.stages:
+                assert kv.add_lane() == li
         self.record_logits = record_logits
         self.logits_log = []   # (t, rows, positions, logits[M, V] np) when recording
         self.ids_log = []      # (t, rows, ids np)
         self.t = 0
         self.n_evicted = self.n_prefetched = 0
-        if graphs:  # one graph per 16-row bucket, captured up front
-            for ex, kv in self.stages:
-                for Mb in range(16, self.m_cap + 16, 16):
-                    ex.capture(min(Mb, self.m_cap), kv.compute)
+        if graphs:  # one graph per 16-row bucket and lane, captured up front
+            for li, stages in enumerate(self.lane_stages):
+                for ex, kv in stages:
+                    for Mb in range(16, self.m_cap + 16, 16):
+                        ex.capture(min(Mb, self.m_cap), kv.streams[li])
         self._init_kv(kv_init, prompts, seed)
 
     # ------------------------------------------------------------------ setup
@@ -174,10 +189,10 @@ class DecodeEngine:
     def bucket(self, M):
         return min(self.m_cap, -(-M // 16) * 16) if self.graphs else M
 
-    def _upload_meta(self, rows, positions, tables, stream=None):
+    def _upload_meta(self, rows, positions, tables, stream=None, lane=0):
         """Block tables, positions, seq lens and slots of the step's rows,
         padded to the 16-row bucket with rows aimed at the trash block/slot."""
-        self._fill_meta([tables[r] for r in rows], positions, [self.slot_of[r] for r in rows], stream)
+        self._fill_meta([tables[r] for r in rows], positions, [self.slot_of[r] for r in rows], stream, lane)
 
     def _upload_meta_rows(self, table, positions, M=None, last_slot=None, stream=None):
         """Prefill chunk: every row is a token of one request (its block
@@ -189,7 +204,7 @@ class DecodeEngine:
             slots[-1] = last_slot
         self._fill_meta([table] * n, positions, slots, stream)
 
-    def _fill_meta(self, row_tables, positions, slots, stream=None):
+    def _fill_meta(self, row_tables, positions, slots, stream=None, lane=0):
         n, mb = len(row_tables), self.max_blocks
         M = self.bucket(n)
         k, buf = self.meta.next()
@@ -198,6 +213,9 @@ class DecodeEngine:
         bt[:] = 0
         for i, tb in enumerate(row_tables):
             bt[i, :len(tb)] = tb
+        # physical blocks the step reads/writes (rows' blocks up to their position)
+        nb = np.asarray(positions, dtype=np.int64) // 16 + 1
+        self._last_used_blocks = bt[:n][np.arange(mb)[None, :] < nb[:, None]].astype(np.int64)
         bt[n:, 0] = self.trash_block
         o = M * mb
         a[o:o + n] = positions
@@ -214,8 +232,8 @@ class DecodeEngine:
         base = self.meta.dev_ptrs[k]
         srcs = (_C.C.c_void_p * 5)(base, base + 4 * o, base + 4 * (o + M), base + 4 * (o + 2 * M), base + 4 * wo)
         counts = (_C.C.c_int * 5)(M * mb, M, M, M, wn)
-        for ex, kv in self.stages:
-            s = kv.compute if stream is None else stream
+        for ex, kv in self.lane_stages[lane]:
+            s = kv.streams[lane] if stream is None else stream
             dsts = (_C.C.c_void_p * 5)(ex.block_table.data_ptr(), ex.positions.data_ptr(), ex.seq_lens.data_ptr(),
                                        ex.slots.data_ptr(), ex.aws.work.data_ptr())
             _C.call("pm_meta_upload", 5, dsts, srcs, counts, _C.C.c_void_p(s.cuda_stream))
@@ -224,26 +242,54 @@ class DecodeEngine:
             evs.append(ev)
         self.meta.events[k] = evs
 
-    def _forward_all(self, n, kv_tokens=0):
-        """Run the stages in order on their compute streams (single process:
-        stage s+1 waits for stage s's activations via an event)."""
+    def _forward_all(self, n, kv_tokens=0, lane=0):
+        """Run the stages in order on the lane's compute streams (single
+        process: stage s+1 waits for stage s's activations via an event)."""
         M = self.bucket(n)
+        stages = self.lane_stages[lane]
         prev_ev = None
-        for si, (ex, kv) in enumerate(self.stages):
+        for si, (ex, kv) in enumerate(stages):
+            st = kv.streams[lane]
             if prev_ev is not None:
-                kv.compute.wait_event(prev_ev)
-            with torch.cuda.stream(kv.compute):
+                st.wait_event(prev_ev)
+            with torch.cuda.stream(st):
                 if si > 0:
-                    ex.resid[:M].copy_(self.stages[si - 1][0].resid[:M])
-                ex.run(M, kv.compute, graphs=self.graphs, kv_tokens=kv_tokens)
-                if si == len(self.stages) - 1 and len(self.stages) > 1:
+                    ex.resid[:M].copy_(stages[si - 1][0].resid[:M])
+                ex.run(M, st, graphs=self.graphs, kv_tokens=kv_tokens)
+                if si == len(stages) - 1 and len(stages) > 1:
                     # greedy ids back to stage 0's token table (the last->first hop)
-                    first = self.stages[0][0]
-                    first.tok_table.copy_(ex.tok_table)
+                    stages[0][0].tok_table.copy_(ex.tok_table)
             prev_ev = torch.cuda.Event()
-            prev_ev.record(kv.compute)
-        if len(self.stages) > 1:
-            self.stages[0][1].compute.wait_event(prev_ev)
+            prev_ev.record(st)
+        if len(stages) > 1:
+            stages[0][1].streams[lane].wait_event(prev_ev)
+
+    # ------------------------------------------------------------------ lanes
+    def lane_of(self, t: int) -> int:
+        return t % self.lanes
+
+    def last_executor(self, t: int):
+        """The last stage's executor that ran step ``t`` (its out_ids/logits)."""
+        return self.lane_stages[self.lane_of(t)][-1][0]
+
+    def begin_region(self, ev):
+        """Record ``ev`` on lane 0's first-stage stream; every other lane's
+        streams wait for it (start of a timed region)."""
+        ev.record(self.stages[0][1].streams[0])
+        for ex, kv in self.stages:
+            for st in kv.streams:
+                st.wait_event(ev)
+
+    def end_region(self, ev):
+        """Record ``ev`` after all work of every lane (end of a timed region)."""
+        s0 = self.stages[0][1].streams[0]
+        for ex, kv in self.stages:
+            for st in kv.streams:
+                if st is not s0:
+                    e = torch.cuda.Event()
+                    e.record(st)
+                    s0.wait_event(e)
+        ev.record(s0)
 
     def step(self) -> StepWork:
         work = self.control.step()
@@ -253,22 +299,25 @@ class DecodeEngine:
         M = len(work.rows)
         self.n_evicted += len(work.evicted) + len(work.relief_evicted)
         self.n_prefetched += len(work.prefetch)
+        lane = self.lane_of(t)
+        stages = self.lane_stages[lane]
         recs = []
         info = {"plan": work.plan, "batch_tokens": work.batch_tokens, "completed": list(work.completed),
                 "resident_tokens": self.control.resident_tokens, "capacity_tokens": self.control.capacity_tokens}
-        for ex, kv in self.stages:
-            rec = {"t": t, "M": M, "info": info}
+        for ex, kv in stages:
+            rec = {"t": t, "M": M, "info": info, "stream": kv.streams[lane], "serialize": self.serialize_lanes}
             kv.prefetch(t, work, rec)
             recs.append(rec)
-        self._upload_meta(work.rows, work.positions, work.tables)
-        for (ex, kv), rec in zip(self.stages, recs):
+        self._upload_meta(work.rows, work.positions, work.tables, lane=lane)
+        for (ex, kv), rec in zip(stages, recs):
+            rec["used_blocks"] = self._last_used_blocks
             kv.before_compute(t, work, rec)
-        self._forward_all(M, kv_tokens=sum(work.positions) + M)
-        for (ex, kv), rec in zip(self.stages, recs):
+        self._forward_all(M, kv_tokens=sum(work.positions) + M, lane=lane)
+        for (ex, kv), rec in zip(stages, recs):
             kv.after_compute(t, rec)
             kv.offload(t, work, rec)
         if self.record_logits and M:
-            last = self.stages[-1][0]
+            last = stages[-1][0]
             torch.cuda.synchronize()
             self.logits_log.append((t, list(work.rows), list(work.positions), last.logits[:M].cpu().numpy()))
             self.ids_log.append((t, list(work.rows), last.out_ids[:M].cpu().numpy().copy()))

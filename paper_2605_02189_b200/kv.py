@@ -68,6 +68,7 @@ class KvEngine:
         self.dev = device
         lo, hi = torch.cuda.Stream.priority_range()
         self.compute = torch.cuda.Stream(device=device, priority=hi)
+        self.streams = [self.compute]   # one compute stream per lane (micro-batch in flight)
         self.h2d = torch.cuda.Stream(device=device, priority=lo)
         self.d2h = torch.cuda.Stream(device=device, priority=lo)
         self.timing = timing
@@ -82,6 +83,15 @@ class KvEngine:
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self.block_last_d2h = np.full(executor.pool_blocks, -1, dtype=np.int64)
+        # last step whose compute read or wrote each block: with several lanes
+        # (micro-batches in flight on different streams) a block freed by one
+        # step and reused by the next needs an explicit compute -> compute edge
+        self.block_last_compute = np.full(executor.pool_blocks, -1, dtype=np.int64)
+
+    def add_lane(self) -> int:
+        lo, hi = torch.cuda.Stream.priority_range()
+        self.streams.append(torch.cuda.Stream(device=self.dev, priority=hi))
+        return len(self.streams) - 1
 
     def _event(self):
         return torch.cuda.Event(enable_timing=self.timing)
@@ -102,9 +112,10 @@ class KvEngine:
                 src.append(base + lb * bb)
                 targets.add(pb)
         s = self.h2d
-        prev = self.compute_done.get(t - 1)
+        last_c = int(self.block_last_compute[list(targets)].max())
+        prev = self.compute_done.get(last_c)
         if prev is not None:
-            s.wait_event(prev)            # reused blocks were last read by step t-1
+            s.wait_event(prev)            # the reused blocks' last reader (normally step t-1)
         # the host copy must hold the requests' last token, and no offload may
         # still be reading a block this copy overwrites
         dep = max((self.last_write.get(rid, -1) for rid, _, _ in work.prefetch), default=-1)
@@ -131,13 +142,25 @@ class KvEngine:
 
     # -- compute ordering -----------------------------------------------------------
     def before_compute(self, t: int, work, rec: dict):
-        s = self.compute
+        s = rec.get("stream", self.compute)
         if self.timing:
             rec["ready"] = self._event()
             rec["ready"].record(s)
         ev = self.h2d_done.get(t - 1)
         if ev is not None:
             s.wait_event(ev)              # batch i's newest members arrived with plan t-1
+        if rec.get("serialize"):
+            ev = self.compute_done.get(t - 1)
+            if ev is not None:
+                s.wait_event(ev)
+        # blocks this step touches that another lane's step touched last
+        used = rec.get("used_blocks")
+        if used is not None and len(used):
+            dep = int(self.block_last_compute[used].max())
+            ev = self.compute_done.get(dep)
+            if ev is not None and dep != t:
+                s.wait_event(ev)
+            self.block_last_compute[used] = t
         # a growth block handed out this step may still be read by an offload
         grow = [work.tables[r][p // 16] for r, p in zip(work.rows, work.positions) if p % 16 == 0]
         if grow:
@@ -151,7 +174,7 @@ class KvEngine:
 
     def after_compute(self, t: int, rec: dict):
         done = self._event()
-        done.record(self.compute)
+        done.record(rec.get("stream", self.compute))
         rec["end"] = done
         self.compute_done[t] = done
 

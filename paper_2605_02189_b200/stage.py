@@ -60,6 +60,25 @@ class StageExecutor:
         self.lm_head_logical = head["lm_head"] if (last and keep_logical) else None
         self.rope = torch.from_numpy(rope_table(s, max_pos)).to(device)
 
+        b16, i32 = torch.bfloat16, torch.int32
+        # KV pool (block-first, token-major inside a block) -- shared by every lane
+        self.tok_elems = self.L_s * 2 * s.Hkv * s.hd
+        self.tok_bytes = self.tok_elems * 2
+        self.block_bytes = 16 * self.tok_bytes
+        self.pool_blocks = pool_blocks
+        self.pool = torch.zeros(pool_blocks * 16 * self.tok_elems, dtype=b16, device=device)
+        self.pool_map = ops.pool_tmap(self.pool, self.L_s, s.Hkv, s.hd)
+        # greedy-token table indexed by request slot -- shared by every lane
+        self.tok_table = torch.zeros(n_slots, dtype=i32, device=device)
+        _C.call("pm_prepare_gemm")
+        _C.call("pm_prepare_attention")
+        self._alloc_lane()
+
+    def _alloc_lane(self):
+        """Per-lane state: activations, step metadata, workspaces, graphs.  A
+        lane is one micro-batch in flight; clone_lane() gives a second one
+        that shares the weights, the KV pool and the token table."""
+        s, m_cap, device = self.spec, self.m_cap, self.dev
         f32, b16, i32 = torch.float32, torch.bfloat16, torch.int32
         self.resid = torch.zeros(m_cap, s.d, dtype=f32, device=device)
         self.xn = torch.zeros(m_cap, s.d, dtype=b16, device=device)
@@ -70,31 +89,30 @@ class StageExecutor:
         self.xn_maps = ops.activation_maps(self.xn)
         self.attn_maps = ops.activation_maps(self.attn)
         self.act_maps = ops.activation_maps(self.act)
-        # KV pool (block-first, token-major inside a block)
-        self.tok_elems = self.L_s * 2 * s.Hkv * s.hd
-        self.tok_bytes = self.tok_elems * 2
-        self.block_bytes = 16 * self.tok_bytes
-        self.pool_blocks = pool_blocks
-        self.pool = torch.zeros(pool_blocks * 16 * self.tok_elems, dtype=b16, device=device)
-        self.pool_map = ops.pool_tmap(self.pool, self.L_s, s.Hkv, s.hd)
-        # per-step metadata (device) and its pinned host staging
-        self.block_table = torch.zeros(m_cap, max_blocks, dtype=i32, device=device)
+        self.block_table = torch.zeros(m_cap, self.max_blocks, dtype=i32, device=device)
         self.positions = torch.zeros(m_cap, dtype=i32, device=device)
         self.seq_lens = torch.ones(m_cap, dtype=i32, device=device)
         self.slots = torch.zeros(m_cap, dtype=i32, device=device)
         self.meta_dev = [self.block_table, self.positions, self.seq_lens, self.slots]
-        self.tok_table = torch.zeros(n_slots, dtype=i32, device=device)
         self.prefill_tokens = torch.zeros(m_cap, dtype=i32, device=device)
         self.out_ids = torch.zeros(m_cap, dtype=i32, device=device)
         self.logits = None
         self.graphs = {}
-        _C.call("pm_prepare_gemm")
-        _C.call("pm_prepare_attention")
-        # workspaces
-        lins = [x[k] for x in self.W for k in ("qkv", "o", "gu", "down")] + ([self.lm_head] if last else [])
+        lins = [x[k] for x in self.W for k in ("qkv", "o", "gu", "down")] + ([self.lm_head] if self.last else [])
         self.gws = ops.GemmWorkspace(m_cap, ops.GemmWorkspace.floats_needed(lins, m_cap),
-                                     max(l.n_units for l in lins), self.lm_head.n_units if last else 1, device)
-        self.aws = ops.AttnWorkspace(m_cap, s.Hkv, s.hd, max_blocks, device)
+                                     max(l.n_units for l in lins), self.lm_head.n_units if self.last else 1, device)
+        self.aws = ops.AttnWorkspace(m_cap, s.Hkv, s.hd, self.max_blocks, device)
+
+    def clone_lane(self) -> "StageExecutor":
+        """A second executor over the same weights, KV pool and token table
+        with its own activations/metadata/workspaces/graphs, so two
+        micro-batches can be in flight on two streams."""
+        import copy
+        twin = copy.copy(self)
+        twin._alloc_lane()
+        if self.logits is not None:
+            twin.enable_logits()
+        return twin
 
     # ------------------------------------------------------------------ views
     def pool_view(self):

@@ -88,3 +88,24 @@ for _ in range(K):
         break
     n += 1
 print(f"control plane alone: {1e3 * (time.perf_counter() - t0) / max(n, 1):.3f} ms/step")
+# two micro-batches in flight: two graphs of the same bucket replayed on two
+# streams concurrently (timing only -- they share activation buffers)
+g2 = torch.cuda.CUDAGraph()
+s2 = torch.cuda.Stream(priority=torch.cuda.Stream.priority_range()[1])
+with torch.cuda.graph(g2, stream=s2):
+    ex.forward(Mb, s2)
+torch.cuda.synchronize()
+for rep in range(2):
+    a.record(kv.compute)
+    s2.wait_event(a)
+    for _ in range(K):
+        with torch.cuda.stream(kv.compute):
+            g.replay()
+        with torch.cuda.stream(s2):
+            g2.replay()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e2.record(s2)
+    kv.compute.wait_event(e2)
+    b.record(kv.compute)
+    torch.cuda.synchronize()
+    print(f"two streams, bucket {Mb}: {a.elapsed_time(b) / (2 * K):.3f} ms per micro-batch step")
