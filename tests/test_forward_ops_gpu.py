@@ -8,13 +8,14 @@ import torch
 
 from oracle import forward_ref as ref
 from paper_2605_02189_b200 import ops
-from paper_2605_02189_b200.models import QWEN3_8B, TINY, rope_table
+from paper_2605_02189_b200.models import LLAMA3_70B, QWEN3_32B, QWEN3_8B, TINY, rope_table
 from paper_2605_02189_b200.stage import StageExecutor
 
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("spec,pos", [(TINY, 0), (TINY, 37), (QWEN3_8B.with_layers(2), 300)])
+@pytest.mark.parametrize("spec,pos", [(TINY, 0), (TINY, 37), (QWEN3_8B.with_layers(2), 300),
+                                      (QWEN3_32B.with_layers(2), 200), (LLAMA3_70B.with_layers(1), 100)])
 def test_single_token_stage_forward(spec, pos):
     s = spec
     dev = torch.device("cuda")

@@ -9,7 +9,7 @@ import torch
 
 from oracle import forward_ref as ref
 from paper_2605_02189_b200 import ops
-from paper_2605_02189_b200.models import TINY, QWEN3_8B, rope_table
+from paper_2605_02189_b200.models import LLAMA3_70B, QWEN3_32B, QWEN3_8B, TINY, rope_table
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
@@ -107,7 +107,7 @@ def _pool(n_blocks, L_s, Hkv, hd):
     return torch.zeros(n_blocks * 16 * L_s * 2 * Hkv * hd, dtype=torch.bfloat16, device=DEV)
 
 
-@pytest.mark.parametrize("spec", [TINY, QWEN3_8B])
+@pytest.mark.parametrize("spec", [TINY, QWEN3_8B, QWEN3_32B, LLAMA3_70B])   # GQA groups 2, 4, 8, 8
 def test_rope_append_and_paged_attention(spec):
     """Random prefixes scattered over random physical blocks; the current
     token goes through the fused qk-norm/RoPE/append kernel, then attention
