@@ -1,6 +1,6 @@
 """Command-line front end of the B200 decode path:
 
-  python -m paper_2605_02189_b200.cli {decode|prefill|calibrate|report} ...
+  python -m paper_2605_02189_b200.cli {decode|prefill|episode|compare|calibrate|report} ...
 
 Mirrors the reference's ``pipemax-sim`` (REF = reference ``pkg/src/pipemax``,
 cli.py:1-454) for the subcommands that exist on hardware:
@@ -9,6 +9,9 @@ cli.py:1-454) for the subcommands that exist on hardware:
                    writes the trace JSONL and the metrics record (reference
                    schemas, REF pipeline_sim.py:57-96 / 156-216);
 * ``prefill``   -- ``run_prefill`` (layer-wise offload); trace JSONL + makespan;
+* ``episode``   -- ``run_episode`` (prefill <-> decode switching, episode.py);
+* ``compare``   -- the same seeded workload under several policies, CSV of
+                   tokens/s, stall and prefetched fraction (REF cli.py:197-230);
 * ``calibrate`` -- measured (b, L, seconds) samples of this GPU (the CSV the
                    reference's ``calibrate`` reads) and the fitted estimator
                    JSON (REF cli.py:311-327);
@@ -93,6 +96,48 @@ def cmd_calibrate(args) -> int:
     return 0
 
 
+def _episode(args, policy):
+    from .episode import B200Backend, run_episode
+    from .model_core import Request
+    spec, state, cfg, params, reqs, desc = _workload(args)
+    if args.host_tokens:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, cpu_kv_capacity=args.host_tokens * cfg.kv_bytes_per_token)
+    fresh = {r: Request(r, q.input_len, q.output_len) for r, q in reqs.items()}
+    backend = B200Backend(spec, cfg, params, fresh, _prompts(spec, fresh, args.seed), seed=args.seed)
+    m = run_episode(list(fresh.values()), cfg, params, policy=policy, seed=args.seed, backend=backend,
+                    rho_hi=args.rho_hi, horizon=args.horizon)
+    return m.to_record(policy, args.seed)
+
+
+def cmd_episode(args) -> int:
+    """Prefill <-> decode episode on the GPU (REF run_episode)."""
+    record = _episode(args, args.policy)
+    with open(args.metrics, "w") as fh:
+        json.dump(record, fh, indent=2, sort_keys=True)
+        fh.write("\n")
+    print(f"{record['tokens_per_second']:.1f} tokens/s, {record['phase_switches']} phase switches, "
+          f"{record['completed_requests']} completed; metrics -> {args.metrics}")
+    return 0
+
+
+def cmd_compare(args) -> int:
+    """The same seeded workload under several policies (REF cli.py:197-230)."""
+    policies = [p.strip() for p in args.policies.split(",") if p.strip()]
+    rows = []
+    for policy in policies:
+        rec = _episode(args, policy)
+        rows.append((policy, rec["tokens_per_second"], rec["stall_seconds"], rec["mean_prefetched_token_fraction"]))
+    with open(args.out, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["policy", "tokens_per_second", "stall_seconds", "prefetched_token_fraction"])
+        for r in rows:
+            w.writerow([r[0], f"{r[1]:.6f}", f"{r[2]:.6f}", f"{r[3]:.6f}"])
+    for r in rows:
+        print(f"{r[0]}: {r[1]:.3f} tokens/s")
+    return 0
+
+
 def cmd_report(args) -> int:
     """Per-iteration decode series of stage 0 (REF cli.py:362-397)."""
     rows = []
@@ -159,6 +204,20 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--samples", default="samples.csv")
     p.add_argument("--out", default="estimator.json")
     p.set_defaults(fn=cmd_calibrate)
+    for name, fn, hlp in (("episode", cmd_episode, "prefill <-> decode episode (run_episode) on the GPU"),
+                          ("compare", cmd_compare, "the same workload under several policies")):
+        p = sub.add_parser(name, help=hlp)
+        _workload_args(p)
+        p.add_argument("--host-tokens", type=int, default=0, help="host KV capacity in tokens (0: unbounded)")
+        p.add_argument("--rho-hi", type=float, default=0.9)
+        p.add_argument("--horizon", type=int, default=None)
+        if name == "episode":
+            p.add_argument("--policy", default="dynamic")
+            p.add_argument("--metrics", default="episode.json")
+        else:
+            p.add_argument("--policies", default="dynamic,no_prefetch,static:0.5")
+            p.add_argument("--out", default="compare.csv")
+        p.set_defaults(fn=fn)
     p = sub.add_parser("report", help="per-iteration decode series from a trace")
     p.add_argument("--trace", required=True)
     p.add_argument("--out", default="report.csv")

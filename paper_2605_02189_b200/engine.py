@@ -264,6 +264,19 @@ class DecodeEngine:
         if len(stages) > 1:
             stages[0][1].streams[lane].wait_event(prev_ev)
 
+    def start_phase(self, control: DecodeControl):
+        """Begin a new decode phase with ``control`` (episode.py): the
+        weights, KV pool, host replicas, token table, lanes and graphs stay;
+        the resident requests' KV is loaded from their host replicas into the
+        blocks the new control plane assigned."""
+        torch.cuda.synchronize()
+        self.control = control
+        self.t = 0
+        for ex, kv in self.stages:
+            kv.reset_phase()
+            kv.load_resident(control.alloc.tables)
+        torch.cuda.synchronize()
+
     # ------------------------------------------------------------------ lanes
     def lane_of(self, t: int) -> int:
         return t % self.lanes

@@ -88,6 +88,36 @@ class KvEngine:
         # step and reused by the next needs an explicit compute -> compute edge
         self.block_last_compute = np.full(executor.pool_blocks, -1, dtype=np.int64)
 
+    def reset_phase(self):
+        """New decode phase (episode.py): step numbers restart at 0, so the
+        per-step event maps and block histories start empty (the caller
+        synchronized the device)."""
+        self.last_write.clear()
+        self.d2h_done.clear()
+        self.compute_done.clear()
+        self.h2d_done.clear()
+        self.block_last_d2h[:] = -1
+        self.block_last_compute[:] = -1
+
+    def load_resident(self, tables: dict):
+        """Bulk H2D of resident requests' KV (host replica -> their blocks)
+        at the start of a decode phase (REF run_episode's initial-residency
+        load, pipeline_sim.py:732-739); returns bytes."""
+        bb = self.block_bytes
+        dst, src = [], []
+        for rid in sorted(tables):
+            base = self.rep.offset(self.slot_of[rid])
+            for lb, pb in enumerate(tables[rid]):
+                dst.append(pb * bb)
+                src.append(base + lb * bb)
+        if dst:
+            d = np.asarray(dst, dtype=np.int64)
+            sr = np.asarray(src, dtype=np.int64)
+            _C.call("pm_copy_pieces", _C.C.c_void_p(self.pool_ptr), _C.C.c_void_p(self.rep.ptr),
+                    d.ctypes.data_as(_C.C.c_void_p), sr.ctypes.data_as(_C.C.c_void_p), len(dst), bb,
+                    _C.C.c_void_p(self.h2d.cuda_stream))
+        return len(dst) * bb
+
     def add_lane(self) -> int:
         lo, hi = torch.cuda.Stream.priority_range()
         self.streams.append(torch.cuda.Stream(device=self.dev, priority=hi))

@@ -48,3 +48,13 @@ def test_decode_then_report(tmp_path):
     assert {"stage_compute_start", "stage_compute_end", "transfer_start", "transfer_end"} <= kinds
     assert cli.main(["report", "--trace", str(tr), "--out", str(rep)]) == 0
     assert len(list(csv.reader(open(rep)))) == 13
+
+
+@pytest.mark.gpu
+def test_compare_policies(tmp_path):
+    out = tmp_path / "c.csv"
+    assert cli.main(["compare", "--requests", "24", "--prompt", "40", "--gen", "8", "--host-tokens", "700",
+                     "--policies", "dynamic,no_prefetch", "--out", str(out)]) == 0
+    rows = list(csv.reader(open(out)))
+    assert rows[0][0] == "policy" and [r[0] for r in rows[1:]] == ["dynamic", "no_prefetch"]
+    assert all(float(r[1]) > 0 for r in rows[1:])
