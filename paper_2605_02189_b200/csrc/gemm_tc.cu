@@ -440,7 +440,7 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
 // ---------------------------------------------------------------- post kernels
 // One CTA per (unit, RC token columns), thread = row of the 256-row unit.
 // RC is chosen per launch so the grid fits in about one wave (launch()).
-constexpr int MAX_SEGS = 8;
+constexpr int MAX_SEGS = 4;
 
 // segment count of stream-K unit `unit` (mirrors get_seg / pm_gemm_max_segments)
 PM_DEV int unit_segments(const GemmArgs& a, int unit, int grid) {
