@@ -51,6 +51,14 @@ def workload(spec_name="qwen3-8b", n_req=256, prompt=512, gen=512, m=2, cap_frac
     return decode_workload(spec_name, n_req, prompt, gen, m, cap_frac, resident_frac)
 
 
+# BASELINE configs run as ONE pipeline stage on this GPU (--config):
+# name, model, batch, prompt, gen, micro-batches, stage index
+STAGE_CONFIGS = {
+    "c3-stage": ("C3", "qwen3-32b", 512, 1024, 64, 8, 3),
+    "c4-stage": ("C4", "llama3-70b", 256, 1024, 64, 8, 3),
+}
+
+
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
     """SM clock and throttle reasons sampled every 20 ms by NVML while the
@@ -175,6 +183,20 @@ def run_ours(args):
                               kv_init="random", timing=True, seed=0)
         eng = peng.eng
         eng.step = peng.step
+    elif args.config in STAGE_CONFIGS:
+        # one pipeline stage of a PP=8 BASELINE config on this GPU: the stage's
+        # layers (a middle stage: no embedding / lm_head), its KV pool and host
+        # replica, the 8-micro-batch rotation; one micro-batch at a time, as a
+        # real stage runs them (no lanes).  tokens/s = the pipeline's steady-
+        # state throughput if every stage ran at this stage's speed.
+        name, spec_name, n_req, prompt, gen, m, stage = STAGE_CONFIGS[args.config]
+        spec, state, cfg, params, reqs, desc = workload(spec_name, n_req, prompt, gen, m)
+        desc["workload"] = (f"{name}: stage {stage} of PP=8 ({spec.layers // 8} of {spec.layers} layers of "
+                            f"{spec_name}), {m} micro-batches x {n_req // m} rows, prompt {prompt}, KV pool capped "
+                            f"at 75% of peak, 25% of requests start in host memory (offload on)")
+        desc["parallelism"] = "pp8-stage"
+        eng = DecodeEngine(spec, state, cfg, params, reqs, pp=8, local_stages=[stage], device=f"cuda:{local}",
+                           kv_init="random", timing=True, seed=rank)
     else:
         spec, state, cfg, params, reqs, desc = workload()
         eng = DecodeEngine(spec, state, cfg, params, reqs, device=f"cuda:{local}", kv_init="random",
@@ -391,6 +413,8 @@ def main():
     ap.add_argument("--no-kernel-timing", dest="kernel_timing", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-calibrate", dest="calibrate", action="store_false")
+    ap.add_argument("--config", default="c2", choices=["c2"] + sorted(STAGE_CONFIGS),
+                    help="c2 (default): BASELINE configs[1] on one GPU; c3-stage / c4-stage: one PP=8 stage")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference"
     if args.impl == "reference":
