@@ -589,13 +589,15 @@ __global__ void __launch_bounds__(256) gemm_resid_norm_kernel(GemmArgs a, int gr
   if (c0 >= tok_end) return;
   const int r = threadIdx.x;
   const int n = wunit * UNIT_ROWS + r;
+  float* o = reinterpret_cast<float*>(a.out);
+  // residual loads issued together with the partial loads (one round trip)
+  float res[RC];
+#pragma unroll
+  for (int j = 0; j < RC; ++j)
+    res[j] = (n < a.n_out && c0 + j < tok_end) ? __ldcg(o + (size_t)(tok_base + c0 + j) * a.ld_out + n) : 0.f;
   float v[RC];
   sum_partials<BN, RC>(a, unit, nseg, c0, r, v);
-  float* o = reinterpret_cast<float*>(a.out);
   if (n < a.n_out) {
-    float res[RC];   // every residual load in flight before the first store
-#pragma unroll
-    for (int j = 0; j < RC; ++j) res[j] = c0 + j < tok_end ? __ldcg(o + (size_t)(tok_base + c0 + j) * a.ld_out + n) : 0.f;
 #pragma unroll
     for (int j = 0; j < RC; ++j)
       if (c0 + j < tok_end) __stcg(o + (size_t)(tok_base + c0 + j) * a.ld_out + n, res[j] + v[j]);
