@@ -242,6 +242,11 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
 
   pdl_trigger();
   if (threadIdx.x == 0) PM_TRACE(0);
+  if (threadIdx.x == 0 && (a.debug & 8) && blockIdx.x < 148) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_gemm_trace[blockIdx.x * 8 + 4] = smid;
+  }
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmap_x);
     // full: own producer's arrive + tx (own weights, both X halves);

@@ -39,3 +39,11 @@ for c in list(range(0, 148, 9)) + [147]:
 for k, name in [(1, "waited"), (2, "last mma"), (3, "epilogue end")]:
     v = rel[:, k][rel[:, k] >= 0]
     print(f"{name:13s} min {v.min()/1e3:7.1f} median {np.median(v)/1e3:7.1f} max {v.max()/1e3:7.1f}")
+
+sm = t[:, 4]
+lm = rel[:, 2]
+order = np.argsort(sm)
+print("last-mma (us) by SM id (sorted):")
+for k in range(0, 148, 8):
+    idx = order[k:k + 8]
+    print(" ".join(f"{int(sm[i]):3d}:{lm[i] / 1e3:5.1f}" for i in idx))
