@@ -344,7 +344,7 @@ def run_ours(args):
         traffic = None   # DRAM bytes per launch of this kind from the committed ncu capture
         try:
             tr = json.load(open(os.path.join(ROOT, "profiles", "traffic_latest.json")))
-            traffic = tr.get("gemm_call" if top == "gemm" else top, {}).get("dram_bytes_per_launch")
+            traffic = tr.get(top, {}).get("dram_bytes_per_launch")
         except Exception:
             pass
         out["roofline"] = {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": peaks["hbm_gbs"],
@@ -352,11 +352,14 @@ def run_ours(args):
                            "algorithmic_bytes_per_launch": d["bytes"] / d["launches"],
                            "peak_source": peaks_src, "share_of_step": d["seconds"] / prof_s,
                            "per_kind": {k: {"launches": v["launches"], "GBps": v["bytes"] / v["seconds"] / 1e9,
+                                            "us_per_launch": v["seconds"] / v["launches"] * 1e6,
                                             "share": v["seconds"] / prof_s} for k, v in summ.items()},
                            "note": f"CUDA events around each launch on the compute stream over {n_prof} further "
                                    "steps of the same run launched eagerly (the timed region replays CUDA "
                                    "graphs); achieved = algorithmic bytes per launch (GEMM: weights once + "
-                                   "activations; attention: the micro-batch's KV once) / launch time"}
+                                   "activations; attention: the micro-batch's KV once) / launch time; "
+                                   "gemm = the stream-K kernel alone, gemm_fixup = its fused fixup/post kernel "
+                                   "(an event recorded between the two launches)"}
     if rank == 0 and args.calibrate:
         # on-box fit of the planner's estimator (REF model_core.py:158-182) from
         # measured iterations of this engine; reported beside the analytic one

@@ -94,6 +94,8 @@ int pm_attn_work_list(const int* seq_lens, int M, int blocks_per_chunk, int hkv,
 int pm_attn_workers(int hd);
 /* one-time kernel attributes; call once per device before CUDA-graph capture */
 int pm_prepare_gemm(void);
+/* profiling: record cudaEvent_t `event` between the next GEMM launch's main and fixup kernels (one-shot) */
+int pm_gemm_split_event(void* event);
 int pm_prepare_attention(void);
 int pm_argmax_reduce(const float* val, const int* idx, int n_tiles, int M, int m_cap, int* out_ids,
                      int* tok_table, const int* slots, void* stream);

@@ -30,6 +30,7 @@ _SIGS = {
     "pm_gemm_qkv_rope": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _I, _I, _P, _U64, _P, _P, _P, _P, _P, _P,
                          _P, _I, _I, _I, _I, _I, _I, _F, _P],
     "pm_gemm_split_units": [_LL, _I, _I],
+    "pm_gemm_split_event": [_P],
     "pm_gemm_max_segments": [_LL, _I, _I],
     "pm_embed": [_P, _P, _P, _P, _I, _I, _P],
     "pm_rmsnorm": [_P, _P, _P, _I, _I, _F, _P],

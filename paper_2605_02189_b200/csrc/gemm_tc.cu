@@ -736,6 +736,11 @@ __global__ void __launch_bounds__(256) gemm_qkv_rope_kernel(GemmArgs a, int grid
 
 enum Post : int { POST_NONE = 0, POST_RESID_NORM = 1, POST_QKV_ROPE = 2 };
 
+// Profiling only (bench.py's per-launch roofline): an event recorded right
+// after the next GEMM main kernel is launched, before its fixup kernel, so
+// the two can be timed separately.  One-shot; null = off.
+cudaEvent_t g_split_event = nullptr;
+
 template <int BN, int NH>
 int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int post, const NormArgs* na,
            const RopeArgs* ra) {
@@ -753,6 +758,10 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int pos
   else
     e = launch_k(gemm_stream_kernel<BN, NH>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, *tx, a);
   if (e != cudaSuccess) return (int)e;
+  if (g_split_event) {
+    cudaEventRecord(g_split_event, st);
+    g_split_event = nullptr;
+  }
   const int G = NH == 1 ? grid / 2 : grid;
   if (post == POST_NONE && (a.max_segs <= 1 || (a.debug & 1))) return 0;
   if (post == POST_RESID_NORM && (a.max_segs <= 1 || (a.debug & 1))) return 0;
@@ -782,6 +791,13 @@ int launch_any(bool pair, const CUtensorMap* tx, GemmArgs a, int grid, cudaStrea
 }
 
 }  // namespace
+
+// Profiling only: record `event` (a cudaEvent_t) between the next GEMM's
+// main kernel and its fixup kernel.
+extern "C" int pm_gemm_split_event(void* event) {
+  g_split_event = reinterpret_cast<cudaEvent_t>(event);
+  return 0;
+}
 
 // Profiling only: copy the last traced launch's stamps ([148][8] u64 ns).
 extern "C" int pm_gemm_trace_read(void* dst) {

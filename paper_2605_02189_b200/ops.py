@@ -21,23 +21,35 @@ class KernelTimer:
     launch's algorithmic HBM bytes."""
 
     def __init__(self):
-        self.pending = []   # (kind, bytes, start_ev, end_ev)
+        self.pending = []   # (kind, bytes, start_ev, end_ev, mid_ev or None)
 
-    def around(self, kind, nbytes, stream, fn):
+    def around(self, kind, nbytes, stream, fn, split=False):
+        """``split``: a GEMM call -- an extra event between its main kernel
+        and its fixup kernel (pm_gemm_split_event) times them separately."""
         s = stream if stream is not None else torch.cuda.current_stream()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        mid = torch.cuda.Event(enable_timing=True) if split else None
         a.record(s)
+        if mid is not None:
+            mid.record(s)   # create the event; re-recorded after the main kernel
+            _C.call("pm_gemm_split_event", C.c_void_p(mid.cuda_event))
         fn()
         b.record(s)
-        self.pending.append((kind, nbytes, a, b))
+        self.pending.append((kind, nbytes, a, b, mid))
 
     def summary(self):
         out = {}
-        for kind, nbytes, a, b in self.pending:
+        for kind, nbytes, a, b, mid in self.pending:
             d = out.setdefault(kind, {"launches": 0, "bytes": 0, "seconds": 0.0})
             d["launches"] += 1
             d["bytes"] += nbytes
-            d["seconds"] += a.elapsed_time(b) * 1e-3
+            if mid is not None:
+                d["seconds"] += a.elapsed_time(mid) * 1e-3
+                p = out.setdefault(kind + "_fixup", {"launches": 0, "bytes": 0, "seconds": 0.0})
+                p["launches"] += 1
+                p["seconds"] += mid.elapsed_time(b) * 1e-3
+            else:
+                d["seconds"] += a.elapsed_time(b) * 1e-3
         return out
 
 
@@ -185,7 +197,7 @@ class Linear:
         if TIMER is None:
             go()
         else:
-            TIMER.around("gemm", kind_bytes, stream, go)
+            TIMER.around("gemm", kind_bytes, stream, go, split=True)
 
     def __call__(self, x_maps: dict, m_tok: int, epilogue: int, out, ld_out: int, ws: GemmWorkspace,
                  stream=None, prefetch=None):
