@@ -63,7 +63,8 @@ struct GemmArgs {
   const uint8_t* pf;  // bytes the NEXT operation streams first: prefetched into L2 during this tail
   unsigned long long pf_bytes;
   long long total;    // units * tok_tiles * kb
-  int debug;          // profiling only: bit0 skip epilogue math, bit2 skip partial stores, bit3 trace
+  int debug;          // profiling only: bit0 skip epilogue math, bit2 skip partial stores, bit3 trace,
+                      // bit4 skip the fixup/post kernel (bits 5/6/7: only reduce / resid-norm / qkv-rope)
 };
 
 // NH = 128-row halves of the 256-row unit one CTA computes: 2 (a CTA owns the
@@ -445,8 +446,6 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
 // ---------------------------------------------------------------- post kernels
 // One CTA per (unit, RC token columns), thread = row of the 256-row unit.
 // RC is chosen per launch so the grid fits in about one wave (launch()).
-constexpr int MAX_SEGS = 4;
-
 // segment count of stream-K unit `unit` (mirrors get_seg / pm_gemm_max_segments)
 PM_DEV int unit_segments(const GemmArgs& a, int unit, int grid) {
   const long long T = a.total, G = grid;
@@ -456,17 +455,19 @@ PM_DEV int unit_segments(const GemmArgs& a, int unit, int grid) {
 }
 
 // v[j] = sum over the unit's segments (in segment order) of row r, column c0+j.
-// Rounds of MAX_SEGS segments; each round issues all its loads before the
+// Rounds of P segments; each round issues all its loads before the
 // first add (volatile keeps them in flight).
 template <int BN, int RC>
 PM_DEV void sum_partials(const GemmArgs& a, int unit, int nseg, int c0, int r, float (&v)[RC]) {
+  // segments per round: every decode shape's units fit in one round at RC 4
+  constexpr int P = RC <= 4 ? 12 : (RC <= 8 ? 6 : 4);
   const float* part = a.ws + (size_t)unit * a.max_segs * BN * UNIT_ROWS + (size_t)c0 * UNIT_ROWS + r;
 #pragma unroll
   for (int j = 0; j < RC; ++j) v[j] = 0.f;
-  for (int s0 = 0; s0 < nseg; s0 += MAX_SEGS) {
-    float t[MAX_SEGS][RC];
+  for (int s0 = 0; s0 < nseg; s0 += P) {
+    float t[P][RC];
 #pragma unroll
-    for (int s = 0; s < MAX_SEGS; ++s)
+    for (int s = 0; s < P; ++s)
 #pragma unroll
       for (int j = 0; j < RC; ++j) {
         float x = 0.f;
@@ -475,13 +476,13 @@ PM_DEV void sum_partials(const GemmArgs& a, int unit, int nseg, int c0, int r, f
         t[s][j] = x;
       }
 #pragma unroll
-    for (int s = 0; s < MAX_SEGS; ++s)
+    for (int s = 0; s < P; ++s)
 #pragma unroll
       for (int j = 0; j < RC; ++j) asm volatile("" : "+f"(t[s][j]));
 #pragma unroll
     for (int j = 0; j < RC; ++j)
 #pragma unroll
-      for (int s = 0; s < MAX_SEGS; ++s) v[j] += t[s][j];
+      for (int s = 0; s < P; ++s) v[j] += t[s][j];
   }
 }
 
@@ -527,6 +528,121 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) 
   }
 }
 
+// Vectorised variant: a thread owns 4 consecutive rows (16-byte partial
+// loads, 8/4/16-byte epilogue stores) of RC token columns; 64 threads cover
+// the 256-row unit, so one CTA finishes 4 x RC columns.  Same summation order
+// as sum_partials (bit-identical).  Needs n_out % 4 == 0 and ld_out % 4 == 0.
+template <int BN, int RC>
+__global__ void __launch_bounds__(256) gemm_reduce_v4_kernel(GemmArgs a, int grid) {
+  pdl_trigger();
+  pdl_wait();
+  const int unit = blockIdx.x;
+  const int nseg = unit_segments(a, unit, grid);
+  if (nseg == 1) return;
+  const int tok_tile = unit / a.n_units, wunit = unit % a.n_units;
+  const int tok_base = tok_tile * BN;
+  const int tok_end = min(BN, a.m_tok - tok_base);
+  const int c0 = (blockIdx.y * 4 + (threadIdx.x >> 6)) * RC;   // warp-uniform
+  if (c0 >= tok_end) return;
+  const int t = threadIdx.x & 63, lane = threadIdx.x & 31;
+  const int r = 4 * t, n = wunit * UNIT_ROWS + r;
+  const float* part = a.ws + (size_t)unit * a.max_segs * BN * UNIT_ROWS + (size_t)c0 * UNIT_ROWS + r;
+  constexpr int P = 4;
+  float4 v[RC];
+#pragma unroll
+  for (int j = 0; j < RC; ++j) v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s0 = 0; s0 < nseg; s0 += P) {
+    float4 x[P][RC];
+#pragma unroll
+    for (int s = 0; s < P; ++s)
+#pragma unroll
+      for (int j = 0; j < RC; ++j) {
+        float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (s0 + s < nseg)
+          asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
+                       : "l"(part + ((size_t)(s0 + s) * BN + j) * UNIT_ROWS));
+        x[s][j] = y;
+      }
+#pragma unroll
+    for (int j = 0; j < RC; ++j)
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        v[j].x += x[s][j].x;
+        v[j].y += x[s][j].y;
+        v[j].z += x[s][j].z;
+        v[j].w += x[s][j].w;
+      }
+  }
+  const bool full4 = n + 3 < a.n_out;
+#pragma unroll
+  for (int j = 0; j < RC; ++j) {
+    const bool col_ok = c0 + j < tok_end;
+    const size_t row = (size_t)(tok_base + c0 + j) * a.ld_out;
+    switch (a.epilogue) {
+      case EPI_STORE_BF16: {
+        bf16* o = reinterpret_cast<bf16*>(a.out) + row + n;
+        if (col_ok && full4) {
+          *reinterpret_cast<uint2*>(o) = make_uint2(pack_bf16(v[j].x, v[j].y), pack_bf16(v[j].z, v[j].w));
+        } else if (col_ok) {
+          const float e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+          for (int i = 0; i < 4; ++i)
+            if (n + i < a.n_out) o[i] = __float2bfloat16(e[i]);
+        }
+        break;
+      }
+      case EPI_RESID_ADD_F32: {
+        float* o = reinterpret_cast<float*>(a.out) + row + n;
+        if (col_ok && full4) {
+          float4 rr = __ldcg(reinterpret_cast<const float4*>(o));
+          rr.x += v[j].x; rr.y += v[j].y; rr.z += v[j].z; rr.w += v[j].w;
+          __stcg(reinterpret_cast<float4*>(o), rr);
+        } else if (col_ok) {
+          const float e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+          for (int i = 0; i < 4; ++i)
+            if (n + i < a.n_out) o[i] = o[i] + e[i];
+        }
+        break;
+      }
+      case EPI_SILU_MUL: {   // rows (gate, up, gate, up) -> outputs n/2, n/2 + 1
+        bf16* o = reinterpret_cast<bf16*>(a.out) + row + (n >> 1);
+        if (col_ok && full4) {
+          *reinterpret_cast<uint32_t*>(o) = pack_bf16(silu(v[j].x) * v[j].y, silu(v[j].z) * v[j].w);
+        } else if (col_ok) {
+          if (n + 1 < a.n_out) o[0] = __float2bfloat16(silu(v[j].x) * v[j].y);
+          if (n + 3 < a.n_out) o[1] = __float2bfloat16(silu(v[j].z) * v[j].w);
+        }
+        break;
+      }
+      case EPI_LOGITS_ARGMAX: {
+        if (a.out && col_ok) {
+          float* o = reinterpret_cast<float*>(a.out) + row + n;
+          if (full4) {
+            *reinterpret_cast<float4*>(o) = v[j];
+          } else {
+            const float e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+            for (int i = 0; i < 4; ++i)
+              if (n + i < a.n_out) o[i] = e[i];
+          }
+        }
+        // one warp = one 128-row half of the unit (argmax tile 2u + half)
+        const float e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+        float bv = -INFINITY;
+        int bi = n;
+        for (int i = 0; i < 4; ++i)
+          if (n + i < a.n_out && e[i] > bv) { bv = e[i]; bi = n + i; }
+        warp_argmax(bv, bi);
+        if (lane == 0 && col_ok) {
+          const size_t tile = (size_t)(wunit * 2 + (t >> 5)) * a.m_cap + tok_base + c0 + j;
+          a.amax_val[tile] = bv;
+          a.amax_idx[tile] = bi;
+        }
+        break;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- fused post kernels
 // (1) residual GEMM (O / down projection) -> resid += x W^T, then the NEXT
 // RMSNorm of every finished row: the CTA that completes a token row last
@@ -544,45 +660,72 @@ struct NormArgs {
 // d) by the whole CTA (256 threads), one row at a time held in registers:
 // one pass over L2 per row (d <= 256 * 4 * NORM_V4).  Same reduction tree as
 // rmsnorm_kernel, so the result is bit-identical to the unfused norm.
-constexpr int NORM_V4 = 8;   // d <= 8192
-PM_DEV void block_rmsnorm_rows(const float* x, int ld, const int* rows, int nrows, const bf16* w, bf16* y, int d,
-                               float eps) {
-  __shared__ float red[8];
-#pragma unroll 1
-  for (int j = 0; j < nrows; ++j) {
-    float4 v[NORM_V4];
-    float ss = 0.f;
+constexpr int NORM_V4 = 8;   // d <= 8192 (instantiated per width: 4, 5, 8 float4 per thread)
+template <int V4>
+PM_DEV void norm_load_row(const float* x, int d, float4 (&v)[V4]) {
 #pragma unroll
-    for (int i = 0; i < NORM_V4; ++i) {
-      const int c = threadIdx.x + i * 256;
-      v[i] = c < d / 4 ? __ldcg(reinterpret_cast<const float4*>(x + (size_t)rows[j] * ld) + c)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int i = 0; i < NORM_V4; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
-    ss = warp_sum(ss);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-    __syncthreads();
-    float t = (threadIdx.x & 31) < 8 ? red[threadIdx.x & 31] : 0.f;
-    t = __shfl_sync(0xffffffffu, warp_sum(t), 0);
-    const float r = rsqrtf(t / (float)d + eps);
-#pragma unroll
-    for (int i = 0; i < NORM_V4; ++i) {
-      const int c = threadIdx.x + i * 256;
-      if (c < d / 4) {
-        const uint2 ww = reinterpret_cast<const uint2*>(w)[c];
-        uint2 o;
-        o.x = pack_bf16(v[i].x * r * bf16_lo(ww.x), v[i].y * r * bf16_hi(ww.x));
-        o.y = pack_bf16(v[i].z * r * bf16_lo(ww.y), v[i].w * r * bf16_hi(ww.y));
-        reinterpret_cast<uint2*>(y + (size_t)rows[j] * d)[c] = o;
-      }
-    }
-    __syncthreads();  // red[] reused by the next row
+  for (int i = 0; i < V4; ++i) {
+    const int c = threadIdx.x + i * 256;
+    v[i] = c < d / 4 ? __ldcg(reinterpret_cast<const float4*>(x) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
-template <int BN, int RC>
-__global__ void __launch_bounds__(256) gemm_resid_norm_kernel(GemmArgs a, int grid, NormArgs na) {
+// Up to d = 5120 (V4 <= 5) the weight slice is loaded once for all rows and
+// row j+1's loads are in flight while row j is reduced, so the rows cost
+// about one L2 round trip; wider rows go one at a time (register budget:
+// the kernel must keep 4 CTAs per SM to stay one wave).
+template <int V4>
+PM_DEV void block_rmsnorm_rows(const float* x, int ld, const int* rows, int nrows, const bf16* w, bf16* y, int d,
+                               float eps) {
+  constexpr bool PIPE = V4 <= 5;
+  __shared__ float red[2][8];
+  uint2 ww[V4];
+  auto load_w = [&]() {
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const int c = threadIdx.x + i * 256;
+      ww[i] = c < d / 4 ? reinterpret_cast<const uint2*>(w)[c] : make_uint2(0u, 0u);
+    }
+  };
+  if (PIPE) load_w();
+  float4 v[V4], nx[PIPE ? V4 : 1];
+  norm_load_row(x + (size_t)rows[0] * ld, d, v);
+#pragma unroll 1
+  for (int j = 0; j < nrows; ++j) {
+    if constexpr (PIPE) {
+      if (j + 1 < nrows) norm_load_row(x + (size_t)rows[j + 1] * ld, d, nx);
+    } else {
+      if (j > 0) norm_load_row(x + (size_t)rows[j] * ld, d, v);
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < V4; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[j & 1][threadIdx.x >> 5] = ss;   // double-buffered: one barrier per row
+    __syncthreads();
+    float t = (threadIdx.x & 31) < 8 ? red[j & 1][threadIdx.x & 31] : 0.f;
+    t = __shfl_sync(0xffffffffu, warp_sum(t), 0);
+    const float r = rsqrtf(t / (float)d + eps);
+    if (!PIPE) load_w();
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const int c = threadIdx.x + i * 256;
+      if (c < d / 4) {
+        uint2 o;
+        o.x = pack_bf16(v[i].x * r * bf16_lo(ww[i].x), v[i].y * r * bf16_hi(ww[i].x));
+        o.y = pack_bf16(v[i].z * r * bf16_lo(ww[i].y), v[i].w * r * bf16_hi(ww[i].y));
+        reinterpret_cast<uint2*>(y + (size_t)rows[j] * d)[c] = o;
+      }
+    }
+    if constexpr (PIPE) {
+#pragma unroll
+      for (int i = 0; i < V4; ++i) v[i] = nx[i];
+    }
+  }
+}
+
+template <int BN, int RC, int V4>
+__global__ void __launch_bounds__(256, 4) gemm_resid_norm_kernel(GemmArgs a, int grid, NormArgs na) {
   pdl_trigger();
   pdl_wait();
   const int unit = blockIdx.x, c0 = blockIdx.y * RC;
@@ -622,7 +765,7 @@ __global__ void __launch_bounds__(256) gemm_resid_norm_kernel(GemmArgs a, int gr
     }
   }
   __syncthreads();
-  if (n_last) block_rmsnorm_rows(o, a.ld_out, last_rows, n_last, na.w, na.xn, a.n_out, na.eps);
+  if (n_last) block_rmsnorm_rows<V4>(o, a.ld_out, last_rows, n_last, na.w, na.xn, a.n_out, na.eps);
 }
 
 // (2) fused QKV projection -> (Qwen3 q/k RMSNorm) + RoPE + paged KV append.
@@ -736,6 +879,11 @@ __global__ void __launch_bounds__(256) gemm_qkv_rope_kernel(GemmArgs a, int grid
 
 enum Post : int { POST_NONE = 0, POST_RESID_NORM = 1, POST_QKV_ROPE = 2 };
 
+bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && atoi(v);
+}
+
 // Profiling only (bench.py's per-launch roofline): an event recorded right
 // after the next GEMM main kernel is launched, before its fixup kernel, so
 // the two can be timed separately.  One-shot; null = off.
@@ -763,6 +911,9 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int pos
     g_split_event = nullptr;
   }
   const int G = NH == 1 ? grid / 2 : grid;
+  if ((a.debug & 16) || ((a.debug & 32) && post == POST_NONE) || ((a.debug & 64) && post == POST_RESID_NORM) ||
+      ((a.debug & 128) && post == POST_QKV_ROPE))
+    return 0;
   if (post == POST_NONE && (a.max_segs <= 1 || (a.debug & 1))) return 0;
   if (post == POST_RESID_NORM && (a.max_segs <= 1 || (a.debug & 1))) return 0;
   // columns per post CTA (4: measured best for the decode shapes)
@@ -775,7 +926,14 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int pos
     const dim3 pg((unsigned)units, BN / R);
     if (post == POST_QKV_ROPE)   // every unit (whole ones read the stored bf16)
       return (int)launch_k(gemm_qkv_rope_kernel<BN, R>, pg, dim3(256), 0, st, a, G, *ra);
-    if (post == POST_RESID_NORM) return (int)launch_k(gemm_resid_norm_kernel<BN, R>, pg, dim3(256), 0, st, a, G, *na);
+    if (post == POST_RESID_NORM) {   // norm width: float4s per thread of the d-wide row
+      if (a.n_out <= 1024 * 4) return (int)launch_k(gemm_resid_norm_kernel<BN, R, 4>, pg, dim3(256), 0, st, a, G, *na);
+      if (a.n_out <= 1024 * 5) return (int)launch_k(gemm_resid_norm_kernel<BN, R, 5>, pg, dim3(256), 0, st, a, G, *na);
+      return (int)launch_k(gemm_resid_norm_kernel<BN, R, NORM_V4>, pg, dim3(256), 0, st, a, G, *na);
+    }
+    static const bool scalar = getenv_flag("PM_POST_SCALAR");   // A/B: thread-per-row kernel
+    if (BN >= 4 * R && a.n_out % 4 == 0 && a.ld_out % 4 == 0 && !scalar)
+      return (int)launch_k(gemm_reduce_v4_kernel<BN, R>, dim3((unsigned)units, BN / (4 * R)), dim3(256), 0, st, a, G);
     return (int)launch_k(gemm_reduce_kernel<BN, R>, pg, dim3(256), 0, st, a, G);
   };
   if (rc == 2) return go(std::integral_constant<int, 2>{});
@@ -908,7 +1066,7 @@ extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, i
   auto st = reinterpret_cast<cudaStream_t>(stream);
   const int post = (na.n_split > 0 && !(a.debug & 1)) ? POST_RESID_NORM : POST_NONE;
   rc = dispatch_bn(bn, [&](auto c) { return launch_any<decltype(c)::value>(cta_pair, tx, a, grid, st, post, &na); });
-  if (rc || post == POST_RESID_NORM) return rc;
+  if (rc || post == POST_RESID_NORM || (a.debug & 16)) return rc;
   return launch_rmsnorm(resid, norm_w, xn, m_tok, n_out, eps, st);
 }
 

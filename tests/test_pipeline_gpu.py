@@ -18,7 +18,9 @@ def test_pipeline_world1_matches_engine():
         if ref.step() is None:
             break
     torch.cuda.synchronize()
-    want = ref.stages[0][0].tok_table.clone()
+    # real request slots only: the trailing trash slot takes whatever the
+    # graph bucket's padding rows write (undefined by design)
+    want = ref.stages[0][0].tok_table[:ref.trash_slot].clone()
     # same scenario through the pipeline driver (prefill seeds the same KV)
     spec2, eng2, reqs2, prompts2 = build(graphs=True)
     # wrap the prefilled engine exactly as PipelineEngine does for its stage
@@ -37,4 +39,4 @@ def test_pipeline_world1_matches_engine():
             break
     pr.finish()
     torch.cuda.synchronize()
-    assert torch.equal(ex.tok_table, want)
+    assert torch.equal(ex.tok_table[:eng2.trash_slot], want)
