@@ -877,6 +877,109 @@ __global__ void __launch_bounds__(256) gemm_qkv_rope_kernel(GemmArgs a, int grid
   }
 }
 
+// Vectorised variant: thread = 4 consecutive features of one head (the
+// unfused qkv_rope_append_kernel's lane layout: feature = lane * 4 + e, so
+// for hd = 128 the result is bit-identical to the unfused path) x 1 token
+// column; 64 threads span the 256-row unit, a CTA finishes 4 columns.  The
+// head's norm and the RoPE partner are shuffles within its HL = hd / 4 lanes.
+template <int BN, int HD>
+__global__ void __launch_bounds__(256) gemm_qkv_rope_v4_kernel(GemmArgs a, int grid, RopeArgs ra) {
+  constexpr int HL = HD / 4;                       // lanes per head (32 or 16)
+  pdl_trigger();
+  const int unit = blockIdx.x;
+  const int tok_tile = unit / a.n_units, wunit = unit % a.n_units;
+  const int tok_base = tok_tile * BN;
+  const int tok_end = min(BN, a.m_tok - tok_base);
+  const int c = blockIdx.y * 4 + (threadIdx.x >> 6);   // warp-uniform column
+  if (c >= tok_end) return;
+  const int nseg = unit_segments(a, unit, grid);
+  const int t = threadIdx.x & 63, lane = threadIdx.x & 31;
+  const int r = 4 * t, n = wunit * UNIT_ROWS + r;
+  const bool row_ok = n < a.n_out;                 // n_out % hd == 0: a head is all in or all out
+  const int hg = n / HD, d = n % HD;               // global head, first dim
+  const bool is_q = hg < ra.H, is_k = !is_q && hg < ra.H + ra.Hkv;
+  const bf16* nw = is_q ? ra.qn_w : (is_k ? ra.kn_w : nullptr);
+  const int m = tok_base + c;
+  // step metadata (written before the step's chain; not a dependent launch) ahead of the wait
+  const int pos = ra.positions[m];
+  const int fi = (lane & (HL / 2 - 1)) * 4;
+  float4 cs = make_float4(0.f, 0.f, 0.f, 0.f), sn = cs;
+  if (is_q || is_k) {
+    cs = *reinterpret_cast<const float4*>(ra.rope + (size_t)pos * HD + fi);
+    sn = *reinterpret_cast<const float4*>(ra.rope + (size_t)pos * HD + HD / 2 + fi);
+  }
+  const int slot_off = is_q ? 0 : ra.block_table[(size_t)m * ra.max_blocks + pos / 16];
+  float w4[4] = {1.f, 1.f, 1.f, 1.f};
+  if (nw) {
+    const uint2 ww = *reinterpret_cast<const uint2*>(nw + d);
+    w4[0] = bf16_lo(ww.x); w4[1] = bf16_hi(ww.x); w4[2] = bf16_lo(ww.y); w4[3] = bf16_hi(ww.y);
+  }
+  pdl_wait();
+  float x[4];
+  if (nseg > 1) {
+    const float* part = a.ws + (size_t)unit * a.max_segs * BN * UNIT_ROWS + (size_t)c * UNIT_ROWS + r;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < nseg; s0 += 12) {
+      float4 y[12];
+#pragma unroll
+      for (int s = 0; s < 12; ++s) {
+        y[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (s0 + s < nseg)
+          asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(y[s].x), "=f"(y[s].y), "=f"(y[s].z), "=f"(y[s].w)
+                       : "l"(part + (size_t)(s0 + s) * BN * UNIT_ROWS));
+      }
+#pragma unroll
+      for (int s = 0; s < 12; ++s) { v.x += y[s].x; v.y += y[s].y; v.z += y[s].z; v.w += y[s].w; }
+    }
+    // the bf16 rounding the stored qkv applies
+    x[0] = __bfloat162float(__float2bfloat16(v.x));
+    x[1] = __bfloat162float(__float2bfloat16(v.y));
+    x[2] = __bfloat162float(__float2bfloat16(v.z));
+    x[3] = __bfloat162float(__float2bfloat16(v.w));
+  } else {
+    uint2 q = make_uint2(0u, 0u);
+    if (row_ok) q = *reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(a.out) + (size_t)m * a.ld_out + n);
+    x[0] = bf16_lo(q.x); x[1] = bf16_hi(q.x); x[2] = bf16_lo(q.y); x[3] = bf16_hi(q.y);
+  }
+  // shuffles run on every lane (a warp may hold heads of different kinds when hd = 64)
+  {
+    float ss = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) ss += x[e] * x[e];
+#pragma unroll
+    for (int o = HL / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (nw) {   // Qwen3 per-head RMSNorm (before RoPE)
+      const float rr = rsqrtf(ss / (float)HD + ra.eps);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) x[e] = x[e] * rr * w4[e];
+    }
+    const bool lo_half = (lane & (HL - 1)) < HL / 2;
+    const float c4[4] = {cs.x, cs.y, cs.z, cs.w}, s4[4] = {sn.x, sn.y, sn.z, sn.w};
+    float y[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float partner = __shfl_xor_sync(0xffffffffu, x[e], HL / 2);
+      y[e] = lo_half ? (x[e] * c4[e] - partner * s4[e]) : (x[e] * c4[e] + partner * s4[e]);
+    }
+    if (is_q || is_k) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) x[e] = y[e];
+    }
+  }
+  if (!row_ok) return;
+  bf16* dst;
+  if (is_q) {
+    dst = ra.q_out + ((size_t)m * ra.H + hg) * HD + d;
+  } else {
+    const int kv = is_k ? 0 : 1;
+    const int g = is_k ? hg - ra.H : hg - ra.H - ra.Hkv;
+    const size_t tok_stride = (size_t)ra.L_s * 2 * ra.Hkv * HD;
+    dst = ra.pool + ((size_t)slot_off * 16 + (pos & 15)) * tok_stride + (((size_t)ra.layer * 2 + kv) * ra.Hkv + g) * HD + d;
+  }
+  *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]));
+}
+
 enum Post : int { POST_NONE = 0, POST_RESID_NORM = 1, POST_QKV_ROPE = 2 };
 
 bool getenv_flag(const char* name) {
@@ -924,14 +1027,20 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int pos
   auto go = [&](auto rcc) -> int {
     constexpr int R = decltype(rcc)::value;
     const dim3 pg((unsigned)units, BN / R);
-    if (post == POST_QKV_ROPE)   // every unit (whole ones read the stored bf16)
+    static const bool scalar = getenv_flag("PM_POST_SCALAR");   // A/B: thread-per-row kernels
+    if (post == POST_QKV_ROPE) {   // every unit (whole ones read the stored bf16)
+      if (!scalar && BN >= 4) {
+        const dim3 g4((unsigned)units, BN / 4);
+        if (ra->hd == 128) return (int)launch_k(gemm_qkv_rope_v4_kernel<BN, 128>, g4, dim3(256), 0, st, a, G, *ra);
+        if (ra->hd == 64) return (int)launch_k(gemm_qkv_rope_v4_kernel<BN, 64>, g4, dim3(256), 0, st, a, G, *ra);
+      }
       return (int)launch_k(gemm_qkv_rope_kernel<BN, R>, pg, dim3(256), 0, st, a, G, *ra);
+    }
     if (post == POST_RESID_NORM) {   // norm width: float4s per thread of the d-wide row
       if (a.n_out <= 1024 * 4) return (int)launch_k(gemm_resid_norm_kernel<BN, R, 4>, pg, dim3(256), 0, st, a, G, *na);
       if (a.n_out <= 1024 * 5) return (int)launch_k(gemm_resid_norm_kernel<BN, R, 5>, pg, dim3(256), 0, st, a, G, *na);
       return (int)launch_k(gemm_resid_norm_kernel<BN, R, NORM_V4>, pg, dim3(256), 0, st, a, G, *na);
     }
-    static const bool scalar = getenv_flag("PM_POST_SCALAR");   // A/B: thread-per-row kernel
     if (BN >= 4 * R && a.n_out % 4 == 0 && a.ld_out % 4 == 0 && !scalar)
       return (int)launch_k(gemm_reduce_v4_kernel<BN, R>, dim3((unsigned)units, BN / (4 * R)), dim3(256), 0, st, a, G);
     return (int)launch_k(gemm_reduce_kernel<BN, R>, pg, dim3(256), 0, st, a, G);
