@@ -768,6 +768,68 @@ __global__ void __launch_bounds__(256, 4) gemm_resid_norm_kernel(GemmArgs a, int
   if (n_last) block_rmsnorm_rows<V4>(o, a.ld_out, last_rows, n_last, na.w, na.xn, a.n_out, na.eps);
 }
 
+// Vectorised variant: thread = 4 consecutive rows x 1 token column (16-byte
+// partial and residual accesses); a CTA finishes 4 columns, like RC = 4.
+template <int BN, int V4>
+__global__ void __launch_bounds__(256, 4) gemm_resid_norm_v4_kernel(GemmArgs a, int grid, NormArgs na) {
+  pdl_trigger();
+  pdl_wait();
+  const int unit = blockIdx.x;
+  const int nseg = unit_segments(a, unit, grid);
+  if (nseg == 1) return;  // whole units were added by the GEMM epilogue and do not count
+  const int tok_tile = unit / a.n_units, wunit = unit % a.n_units;
+  const int tok_base = tok_tile * BN;
+  const int tok_end = min(BN, a.m_tok - tok_base);
+  const int cbase = blockIdx.y * 4;
+  if (cbase >= tok_end) return;            // CTA-uniform
+  const int cg = threadIdx.x >> 6, t = threadIdx.x & 63;
+  const int c = cbase + cg;
+  const bool col_ok = c < tok_end;
+  const int r = 4 * t, n = wunit * UNIT_ROWS + r;
+  float* o = reinterpret_cast<float*>(a.out);
+  float* orow = o + (size_t)(tok_base + c) * a.ld_out + n;
+  const bool ok = col_ok && n < a.n_out;   // n_out % 8 == 0: 4 rows all in or all out
+  float4 res = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (ok) res = __ldcg(reinterpret_cast<const float4*>(orow));
+  if (col_ok) {
+    const float* part = a.ws + (size_t)unit * a.max_segs * BN * UNIT_ROWS + (size_t)c * UNIT_ROWS + r;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < nseg; s0 += 12) {
+      float4 y[12];
+#pragma unroll
+      for (int s = 0; s < 12; ++s) {
+        y[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (s0 + s < nseg)
+          asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(y[s].x), "=f"(y[s].y), "=f"(y[s].z), "=f"(y[s].w)
+                       : "l"(part + (size_t)(s0 + s) * BN * UNIT_ROWS));
+      }
+#pragma unroll
+      for (int s = 0; s < 12; ++s) { v.x += y[s].x; v.y += y[s].y; v.z += y[s].z; v.w += y[s].w; }
+    }
+    if (ok) {
+      res.x += v.x; res.y += v.y; res.z += v.z; res.w += v.w;
+      __stcg(reinterpret_cast<float4*>(orow), res);
+    }
+  }
+  // arrive on each finished row; the last unit to arrive normalises it
+  __shared__ int last_rows[4];
+  __shared__ int n_last;
+  if (threadIdx.x == 0) n_last = 0;
+  __syncthreads();
+  if (threadIdx.x < 4 && cbase + threadIdx.x < tok_end) {
+    const int row = tok_base + cbase + threadIdx.x;
+    int prev;
+    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(prev) : "l"(na.row_cnt + row) : "memory");
+    if (prev == na.n_split - 1) {
+      na.row_cnt[row] = 0;
+      last_rows[atomicAdd(&n_last, 1)] = row;
+    }
+  }
+  __syncthreads();
+  if (n_last) block_rmsnorm_rows<V4>(o, a.ld_out, last_rows, n_last, na.w, na.xn, a.n_out, na.eps);
+}
+
 // (2) fused QKV projection -> (Qwen3 q/k RMSNorm) + RoPE + paged KV append.
 // One CTA per (unit = 256 output features = 256/hd whole heads, RC tokens);
 // thread = feature.  Split units are summed from the partials, whole units
@@ -1035,6 +1097,12 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int pos
         if (ra->hd == 64) return (int)launch_k(gemm_qkv_rope_v4_kernel<BN, 64>, g4, dim3(256), 0, st, a, G, *ra);
       }
       return (int)launch_k(gemm_qkv_rope_kernel<BN, R>, pg, dim3(256), 0, st, a, G, *ra);
+    }
+    if (post == POST_RESID_NORM && !scalar && BN >= 4) {
+      const dim3 g4((unsigned)units, BN / 4);
+      if (a.n_out <= 1024 * 4) return (int)launch_k(gemm_resid_norm_v4_kernel<BN, 4>, g4, dim3(256), 0, st, a, G, *na);
+      if (a.n_out <= 1024 * 5) return (int)launch_k(gemm_resid_norm_v4_kernel<BN, 5>, g4, dim3(256), 0, st, a, G, *na);
+      return (int)launch_k(gemm_resid_norm_v4_kernel<BN, NORM_V4>, g4, dim3(256), 0, st, a, G, *na);
     }
     if (post == POST_RESID_NORM) {   // norm width: float4s per thread of the d-wide row
       if (a.n_out <= 1024 * 4) return (int)launch_k(gemm_resid_norm_kernel<BN, R, 4>, pg, dim3(256), 0, st, a, G, *na);
