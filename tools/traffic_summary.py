@@ -1,7 +1,7 @@
 """Per-kernel-kind DRAM traffic of one decode step from an ncu metrics CSV
 (dram__bytes_read.sum, dram__bytes_write.sum, gpu__time_duration.sum over
 the launches of the last `n` kernels).  Kinds match bench.py's roofline
-kinds: "gemm" = stream-K GEMM + its post kernel, "attention".
+kinds: "gemm" = the stream-K GEMM kernel, "gemm_fixup" = its post kernel, "attention".
 usage: python tools/traffic_summary.py ncu.csv n_last out.json"""
 import collections
 import csv
@@ -22,7 +22,7 @@ def kind(name):
     if "gemm_stream" in name:
         return "gemm"
     if "gemm_" in name:
-        return "gemm_post"
+        return "gemm_fixup"
     if "paged_attn" in name:
         return "attention"
     return "other"
@@ -37,8 +37,8 @@ for d in launches:
 out = {k: {"launches": v["launches"], "dram_bytes_per_launch": v["dram_bytes"] / v["launches"],
            "us_per_launch": v["ns"] / v["launches"] / 1e3} for k, v in agg.items()}
 # bench.py's "gemm" kind times the GEMM call including its post/reduce kernel
-if "gemm" in out and "gemm_post" in agg:
-    g, p = agg["gemm"], agg["gemm_post"]
+if "gemm" in out and "gemm_fixup" in agg:
+    g, p = agg["gemm"], agg["gemm_fixup"]
     out["gemm_call"] = {"launches": g["launches"],
                         "dram_bytes_per_launch": (g["dram_bytes"] + p["dram_bytes"]) / g["launches"]}
 json.dump(out, open(sys.argv[3], "w"), indent=1)
