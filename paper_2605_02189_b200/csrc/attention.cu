@@ -452,6 +452,7 @@ int num_sms() {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (getenv("PM_ATTN_SMS")) sms = atoi(getenv("PM_ATTN_SMS"));   // tuning experiments only
   }
   return sms;
 }

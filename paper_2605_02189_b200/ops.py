@@ -122,7 +122,14 @@ def pack_weight(w: torch.Tensor):
 PAIR_MAX_UNITS = 64   # narrower projections run on 2-CTA clusters (measured: QKV/O/down win, gate/up loses)
 
 
-def gemm_plan(n_units: int, kb: int, m_tok: int, sms: int = SMS):
+# SMs a decode GEMM's stream-K workers span.  Measured on the C2 bench
+# (two lanes in flight): 128 of the 148 SMs is ~1.5 % faster per step than
+# all of them -- the other lane's fixup / attention CTAs start on the 20 free
+# SMs instead of queueing behind the GEMM's drain (PM_GEMM_CTAS overrides).
+GEMM_CTAS = int(__import__("os").environ.get("PM_GEMM_CTAS", "128"))
+
+
+def gemm_plan(n_units: int, kb: int, m_tok: int, sms: int = None):
     """Stream-K geometry of one launch: (bn, grid CTAs, max segments per
     unit, token tiles, pair).  Narrow projections (fewer than
     PAIR_MAX_UNITS 256-row units) use 2-CTA cluster workers -- each CTA
@@ -131,6 +138,7 @@ def gemm_plan(n_units: int, kb: int, m_tok: int, sms: int = SMS):
     segments; wide ones use one CTA per worker.  The k-block ranges depend on
     (units, K, #SMs) only -- not on m_tok for m_tok <= 256 -- which keeps
     results batch-invariant."""
+    sms = GEMM_CTAS if sms is None else sms
     bn = bn_for(m_tok)
     tt = -(-m_tok // bn)
     total = n_units * tt * kb
