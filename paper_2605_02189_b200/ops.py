@@ -119,7 +119,7 @@ def pack_weight(w: torch.Tensor):
     return out, n_pad // UNIT_ROWS
 
 
-PAIR_MAX_UNITS = 64   # narrower projections run on 2-CTA clusters (measured: QKV/O/down win, gate/up loses)
+PAIR_MAX_UNITS = int(__import__("os").environ.get("PM_PAIR_MAX_UNITS", "64"))   # narrower projections run on 2-CTA clusters (measured: QKV/O/down win, gate/up loses)
 
 
 # SMs a decode GEMM's stream-K workers span.  Measured on the C2 bench
