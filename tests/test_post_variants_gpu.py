@@ -24,7 +24,7 @@ def ws_for(lin, m_cap=256):
 g = torch.Generator(device=DEV).manual_seed(11)
 for name, n_out, k, m, epi in [("store", 6144, 4096, 77, ops.EPI_STORE_BF16), ("resid", 4096, 12288, 128, ops.EPI_RESID_ADD),
                                ("silu", 2 * 3072, 4096, 100, ops.EPI_SILU_MUL), ("pad", 640, 8192, 33, ops.EPI_STORE_BF16),
-                               ("logits", 32768, 1024, 50, ops.EPI_LOGITS_ARGMAX)]:
+                               ("logits", 30000, 1024, 50, ops.EPI_LOGITS_ARGMAX)]:
     w = (torch.randn(n_out, k, generator=g, device=DEV) * 0.05).to(torch.bfloat16)
     x = torch.zeros(256, k, device=DEV, dtype=torch.bfloat16)
     x[:m] = torch.randn(m, k, generator=g, device=DEV).to(torch.bfloat16)
