@@ -1241,7 +1241,10 @@ extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, i
               pm_gemm_split_units(a.total, a.kb, cta_pair ? grid / 2 : grid), eps};
   auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   auto st = reinterpret_cast<cudaStream_t>(stream);
-  const int post = (na.n_split > 0 && !(a.debug & 1)) ? POST_RESID_NORM : POST_NONE;
+  // A/B: PM_NORM_SPLIT=1 finishes split units with the plain reduce kernel and
+  // normalises in a separate row-parallel kernel
+  static const bool norm_split = getenv_flag("PM_NORM_SPLIT");
+  const int post = (na.n_split > 0 && !(a.debug & 1) && !norm_split) ? POST_RESID_NORM : POST_NONE;
   rc = dispatch_bn(bn, [&](auto c) { return launch_any<decltype(c)::value>(cta_pair, tx, a, grid, st, post, &na); });
   if (rc || post == POST_RESID_NORM || (a.debug & 16)) return rc;
   return launch_rmsnorm(resid, norm_w, xn, m_tok, n_out, eps, st);
