@@ -63,11 +63,13 @@ int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, in
 /* prefetch/prefetch_bytes: optional region the NEXT operation reads first; it is pulled into L2 while
  * this GEMM drains (keeps HBM busy across the kernel boundary); NULL/0 for none. */
 /* residual projection (O / down) fused with the next RMSNorm: resid += X W^T (fp32), then
- * xn = RMSNorm(resid) * norm_w (bf16) per row; row_counters int[m_cap], zero at rest, left zero */
+ * xn = RMSNorm(resid) * norm_w (bf16) per row; row_counters int[m_cap], zero at rest, left zero.
+ * split_norm = 0: the last unit to finish a row normalises it inside the fixup kernel;
+ * 1: fixup kernel, then a row-parallel RMSNorm kernel (same result, bit for bit) */
 int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
                           int bn, int grid, int cta_pair, float* resid, float* ws, int max_segs, int m_cap, const void* prefetch,
                           unsigned long long prefetch_bytes, const void* norm_w, void* xn, float eps,
-                          int* row_counters, void* stream);
+                          int* row_counters, int split_norm, void* stream);
 /* QKV projection fused with (Qwen3 q/k RMSNorm) + RoPE + paged KV append (pm_qkv_rope_append's contract);
  * qkv_out [m_cap][n_out] bf16 is scratch */
 int pm_gemm_qkv_rope(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok, int bn,

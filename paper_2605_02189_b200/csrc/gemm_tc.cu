@@ -1231,7 +1231,7 @@ extern "C" int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int 
 extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k,
                                      int m_tok, int bn, int grid, int cta_pair, float* resid, float* ws, int max_segs, int m_cap,
                                      const void* prefetch, unsigned long long prefetch_bytes, const void* norm_w,
-                                     void* xn, float eps, int* row_counters, void* stream) {
+                                     void* xn, float eps, int* row_counters, int split_norm, void* stream) {
   GemmArgs a;
   int rc = make_args(a, grid, cta_pair, w_packed, n_out, n_units, k, m_tok, bn, EPI_RESID_ADD_F32, resid, n_out, ws,
                      max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes);
@@ -1241,10 +1241,10 @@ extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, i
               pm_gemm_split_units(a.total, a.kb, cta_pair ? grid / 2 : grid), eps};
   auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   auto st = reinterpret_cast<cudaStream_t>(stream);
-  // A/B: PM_NORM_SPLIT=1 finishes split units with the plain reduce kernel and
-  // normalises in a separate row-parallel kernel
-  static const bool norm_split = getenv_flag("PM_NORM_SPLIT");
-  const int post = (na.n_split > 0 && !(a.debug & 1) && !norm_split) ? POST_RESID_NORM : POST_NONE;
+  // split_norm: finish split units with the plain reduce kernel and normalise in
+  // a separate row-parallel kernel (measured better when nothing overlaps the
+  // arrival chain: one micro-batch in flight)
+  const int post = (na.n_split > 0 && !(a.debug & 1) && !split_norm) ? POST_RESID_NORM : POST_NONE;
   rc = dispatch_bn(bn, [&](auto c) { return launch_any<decltype(c)::value>(cta_pair, tx, a, grid, st, post, &na); });
   if (rc || post == POST_RESID_NORM || (a.debug & 16)) return rc;
   return launch_rmsnorm(resid, norm_w, xn, m_tok, n_out, eps, st);

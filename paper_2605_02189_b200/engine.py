@@ -130,6 +130,10 @@ class DecodeEngine:
             lanes = 2 if (pp == 1 and local_stages is None) else 1
         self.serialize_lanes = False   # True: step t waits for step t-1 (per-kernel timing passes)
         self.lanes = lanes
+        # one micro-batch in flight: nothing overlaps the fused norm's arrival
+        # chain, and fixup + a row-parallel norm kernel measured faster
+        for ex, _ in self.stages:
+            ex.split_norm = lanes == 1
         self.lane_stages = [self.stages]
         for li in range(1, lanes):
             self.lane_stages.append([(ex.clone_lane(), kv) for ex, kv in self.stages])

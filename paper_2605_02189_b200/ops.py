@@ -223,7 +223,7 @@ class Linear:
         self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * out_b, stream, go)
 
     def resid_rmsnorm(self, x_maps: dict, m_tok: int, resid, ws: GemmWorkspace, norm_w, xn, eps: float,
-                      stream=None, prefetch=None):
+                      stream=None, prefetch=None, split_norm: bool = False):
         """resid += x W^T, then xn = RMSNorm(resid) * norm_w -- the residual
         projection fused with the next layer norm (pm_gemm_resid_rmsnorm)."""
         bn, grid, segs, tt, pair = self.plan(m_tok)
@@ -232,7 +232,7 @@ class Linear:
         def go():
             _C.call("pm_gemm_resid_rmsnorm", _ptr(self.packed), x_maps[bn // 2 if pair else bn].ptr, self.n_out, self.n_units, self.k,
                     m_tok, bn, grid, int(pair), _ptr(resid), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, _ptr(norm_w),
-                    _ptr(xn), float(eps), _ptr(ws.row_cnt), _stream(stream))
+                    _ptr(xn), float(eps), _ptr(ws.row_cnt), int(split_norm), _stream(stream))
         self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * (8 + 4 + 2), stream, go)
 
     def qkv_rope(self, x_maps: dict, m_tok: int, qkv, ws: GemmWorkspace, q_out, pool, block_table, positions,

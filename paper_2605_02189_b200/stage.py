@@ -30,6 +30,8 @@ def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor
 
 
 class StageExecutor:
+    split_norm = False   # O/down fixup + separate RMSNorm kernel (set by the engine for one lane)
+
     def __init__(self, spec: ModelSpec, layers: range, *, first: bool, last: bool, m_cap: int,
                  pool_blocks: int, max_blocks: int, n_slots: int, device, seed: int = 0,
                  max_pos: int = 4096, weights=None, keep_logical=False):
@@ -151,12 +153,14 @@ class StageExecutor:
             ops.paged_attention(self.pool_map, self.q, self.block_table, self.seq_lens, self.attn, self.aws,
                                 M, s.H, s.Hkv, s.hd, li, self.L_s, stream, kv_tokens=kv_tokens)
             # O projection + residual + post-attention RMSNorm
-            w["o"].resid_rmsnorm(self.attn_maps, M, self.resid, self.gws, w["mlp_norm"], self.xn, s.eps, stream)
+            w["o"].resid_rmsnorm(self.attn_maps, M, self.resid, self.gws, w["mlp_norm"], self.xn, s.eps, stream,
+                                 split_norm=self.split_norm)
             w["gu"](self.xn_maps, M, ops.EPI_SILU_MUL, self.act, s.ffn, self.gws, stream)
             # down projection + residual + the next norm (next layer's, or the final one)
             nxt = self.W[li + 1]["attn_norm"] if li + 1 < len(self.W) else (self.final_norm if self.last else None)
             if nxt is not None:
-                w["down"].resid_rmsnorm(self.act_maps, M, self.resid, self.gws, nxt, self.xn, s.eps, stream)
+                w["down"].resid_rmsnorm(self.act_maps, M, self.resid, self.gws, nxt, self.xn, s.eps, stream,
+                                        split_norm=self.split_norm)
             else:
                 w["down"](self.act_maps, M, ops.EPI_RESID_ADD, self.resid, s.d, self.gws, stream)
         if self.last:

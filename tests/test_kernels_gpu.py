@@ -184,11 +184,12 @@ def test_rope_append_and_paged_attention(spec):
 
 @pytest.mark.parametrize("n_out,k,m", [(4096, 4096, 128), (512, 256, 7), (8192, 1024, 200), (512, 64, 16),
                                        (4096, 12288, 64)])
-def test_fused_resid_rmsnorm_matches_unfused(n_out, k, m):
+@pytest.mark.parametrize("split_norm", [False, True])
+def test_fused_resid_rmsnorm_matches_unfused(n_out, k, m, split_norm):
     """pm_gemm_resid_rmsnorm == pm_gemm(+resid) then pm_rmsnorm: the residual
     bit-for-bit, the normalised row bit-for-bit (same reduction order), and
     the per-row arrival counters re-armed; (512, 64) splits no unit and takes
-    the separate-norm path."""
+    the separate-norm path, as does split_norm=True."""
     g = torch.Generator(device=DEV).manual_seed(n_out + k + m)
     w = (torch.randn(n_out, k, generator=g, device=DEV) * 0.05).to(torch.bfloat16)
     m_cap = max(256, m)
@@ -204,7 +205,7 @@ def test_fused_resid_rmsnorm_matches_unfused(n_out, k, m):
     xn_fused = torch.zeros_like(xn_ref)
     lin(maps, m, ops.EPI_RESID_ADD, r_ref, n_out, ws)
     ops.rmsnorm(r_ref, nw, xn_ref, m, 1e-6)
-    lin.resid_rmsnorm(maps, m, r_fused, ws, nw, xn_fused, 1e-6)
+    lin.resid_rmsnorm(maps, m, r_fused, ws, nw, xn_fused, 1e-6, split_norm=split_norm)
     torch.cuda.synchronize()
     assert torch.equal(r_fused, r_ref)
     assert torch.equal(xn_fused[:m], xn_ref[:m])
