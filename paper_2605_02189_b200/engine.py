@@ -108,11 +108,14 @@ class DecodeEngine:
         self.graphs = graphs
         self.stages = []
         self.pp = pp
+        if lanes is None:
+            lanes = 2 if (pp == 1 and local_stages is None) else 1
         for s in (range(pp) if local_stages is None else local_stages):
             ex = StageExecutor(spec, stage_layers(spec, pp, s), first=(s == 0), last=(s == pp - 1),
                                m_cap=self.m_cap, pool_blocks=pool_blocks, max_blocks=self.max_blocks,
                                n_slots=len(rids) + 1, device=self.dev, seed=seed, max_pos=self.max_pos,
-                               keep_logical=record_logits)
+                               keep_logical=record_logits,
+                               gemm_sms=ops.GEMM_CTAS_1LANE if lanes == 1 else None)
             if record_logits:
                 ex.enable_logits()
             rep = HostReplica(len(rids), self.max_blocks, ex.block_bytes)
@@ -126,8 +129,6 @@ class DecodeEngine:
         # compute streams with their own activation buffers and graphs, so one
         # step's latency-bound kernels overlap the other's weight streaming.
         # Ordering through the KV pool stays event-based per step (KvEngine).
-        if lanes is None:
-            lanes = 2 if (pp == 1 and local_stages is None) else 1
         self.serialize_lanes = False   # True: step t waits for step t-1 (per-kernel timing passes)
         self.lanes = lanes
         # one micro-batch in flight: nothing overlaps the fused norm's arrival

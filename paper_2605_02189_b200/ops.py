@@ -127,6 +127,9 @@ PAIR_MAX_UNITS = int(__import__("os").environ.get("PM_PAIR_MAX_UNITS", "64"))   
 # all of them -- the other lane's fixup / attention CTAs start on the 20 free
 # SMs instead of queueing behind the GEMM's drain (PM_GEMM_CTAS overrides).
 GEMM_CTAS = int(__import__("os").environ.get("PM_GEMM_CTAS", "128"))
+# ... and with a single micro-batch in flight (per-stage runs): measured C3
+# 2.140 -> 2.122 ms/step at 116 (PM_GEMM_CTAS_1LANE overrides)
+GEMM_CTAS_1LANE = int(__import__("os").environ.get("PM_GEMM_CTAS_1LANE", "116"))
 
 
 def gemm_plan(n_units: int, kb: int, m_tok: int, sms: int = None):
@@ -170,7 +173,7 @@ class GemmWorkspace:
         need = 1
         for lin in linears:
             for m in sorted({min(m_cap, x) for x in (16, 32, 64, 128, 256, m_cap)}):
-                bn, grid, segs, tt, _pair = gemm_plan(lin.n_units, lin.kb, m)
+                bn, grid, segs, tt, _pair = gemm_plan(lin.n_units, lin.kb, m, lin.sms)
                 need = max(need, lin.n_units * tt * segs * bn * UNIT_ROWS)
         return need
 
@@ -185,6 +188,7 @@ class Linear:
         self.packed, self.n_units = pack_weight(weight)
         self.weight_bytes = self.n_out * self.k * 2
         self._plans = {}
+        self.sms = None   # SMs the stream-K workers span (None: GEMM_CTAS)
 
     def launches(self, m_tok) -> int:
         """Kernels one call launches: the stream-K GEMM, plus gemm_reduce when
@@ -194,7 +198,7 @@ class Linear:
     def plan(self, m_tok):
         p = self._plans.get(m_tok)
         if p is None:
-            p = self._plans[m_tok] = gemm_plan(self.n_units, self.kb, m_tok)
+            p = self._plans[m_tok] = gemm_plan(self.n_units, self.kb, m_tok, self.sms)
         return p
 
     @staticmethod

@@ -34,11 +34,12 @@ class StageExecutor:
 
     def __init__(self, spec: ModelSpec, layers: range, *, first: bool, last: bool, m_cap: int,
                  pool_blocks: int, max_blocks: int, n_slots: int, device, seed: int = 0,
-                 max_pos: int = 4096, weights=None, keep_logical=False):
+                 max_pos: int = 4096, weights=None, keep_logical=False, gemm_sms: int = None):
         self.spec, self.layers = spec, list(layers)
         self.first, self.last = first, last
         self.L_s = len(self.layers)
         self.m_cap, self.max_blocks, self.dev = m_cap, max_blocks, device
+        self.gemm_sms = gemm_sms
         s = spec
         self.logical = [] if keep_logical else None
         self.W = []
@@ -101,6 +102,8 @@ class StageExecutor:
         self.logits = None
         self.graphs = {}
         lins = [x[k] for x in self.W for k in ("qkv", "o", "gu", "down")] + ([self.lm_head] if self.last else [])
+        for lin in lins:   # before the workspace is sized from the plans
+            lin.sms = self.gemm_sms
         self.gws = ops.GemmWorkspace(m_cap, ops.GemmWorkspace.floats_needed(lins, m_cap),
                                      max(l.n_units for l in lins), self.lm_head.n_units if self.last else 1, device)
         self.aws = ops.AttnWorkspace(m_cap, s.Hkv, s.hd, self.max_blocks, device)
