@@ -86,7 +86,10 @@ int pm_qkv_rope_append(const void* qkv, void* q_out, void* pool, const int* bloc
 int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_table, const int* seq_lens,
                        const int* work, void* out, float* ws_o, float* ws_ml, int* counters, int M, int H,
                        int Hkv, int hd,
-                       int layer, int L_s, int max_blocks, int max_chunks, int blocks_per_chunk, void* stream);
+                       int layer, int L_s, int max_blocks, int max_chunks, int blocks_per_chunk, int cfg,
+                       void* stream);
+/* cfg: warps x KV-ring stages per SM (0: 6x4, 1: 12x2, 2: 8x3, 3: 4x2 at 2 CTAs/SM; -1: default);
+ * the work list must be built for pm_attn_workers_cfg(hd, cfg) warps.  Results do not depend on it. */
 int pm_attn_blocks_per_split(void);
 /* host: a step's attention work list -- non-empty (chunk, row) pairs chunk-major, stably sorted by size
  * descending, odd rounds of workers/hkv entries reversed; work[0] = count, entry j = {(chunk << 16) | row,
@@ -94,6 +97,7 @@ int pm_attn_blocks_per_split(void);
 int pm_attn_work_list(const int* seq_lens, int M, int blocks_per_chunk, int hkv, int workers, int* work);
 /* warps of a full attention launch on the current device (the `workers` above) */
 int pm_attn_workers(int hd);
+int pm_attn_workers_cfg(int hd, int cfg);
 /* one-time kernel attributes; call once per device before CUDA-graph capture */
 int pm_prepare_gemm(void);
 /* profiling: record cudaEvent_t `event` between the next GEMM launch's main and fixup kernels (one-shot) */

@@ -462,8 +462,8 @@ int workers_cfg() {
   return num_sms() * (per_sm > 0 ? per_sm : 1) * WARPS;
 }
 template <int HD>
-int attn_workers() {
-  switch (attn_cfg()) {
+int attn_workers(int cfg) {
+  switch (cfg < 0 ? attn_cfg() : cfg) {
     case 0: return workers_cfg<HD, 6, 4>();
     case 2: return workers_cfg<HD, 8, 3>();
     case 3: return workers_cfg<HD, 4, 2>();
@@ -472,8 +472,8 @@ int attn_workers() {
 }
 
 template <int HD>
-int launch_attn(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
-  switch (attn_cfg()) {
+int launch_attn(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st, int cfg) {
+  switch (cfg < 0 ? attn_cfg() : cfg) {
     case 0: return launch_cfg<HD, 6, 4>(tm, a, st);
     case 2: return launch_cfg<HD, 8, 3>(tm, a, st);
     case 3: return launch_cfg<HD, 4, 2>(tm, a, st);
@@ -492,7 +492,7 @@ int launch_attn(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
 extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_table,
                                   const int* seq_lens, const int* work, void* out, float* ws_o, float* ws_ml,
                                   int* counters, int M, int H, int Hkv, int hd, int layer, int L_s, int max_blocks,
-                                  int max_chunks, int blocks_per_chunk, void* stream) {
+                                  int max_chunks, int blocks_per_chunk, int cfg, void* stream) {
   (void)L_s;
   if (M == 0) return 0;
   const int G = H / Hkv;
@@ -503,8 +503,8 @@ extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int*
              1.4426950408889634f / sqrtf((float)hd), getenv("PM_ATTN_DEBUG") ? atoi(getenv("PM_ATTN_DEBUG")) : 0};
   auto tm = reinterpret_cast<const CUtensorMap*>(tmap_kv);
   auto st = reinterpret_cast<cudaStream_t>(stream);
-  if (hd == 128) return launch_attn<128>(tm, a, st);
-  if (hd == 64) return launch_attn<64>(tm, a, st);
+  if (hd == 128) return launch_attn<128>(tm, a, st, cfg);
+  if (hd == 64) return launch_attn<64>(tm, a, st, cfg);
   return (int)cudaErrorInvalidValue;
 }
 
@@ -518,10 +518,15 @@ extern "C" int pm_attn_blocks_per_split(void) {
   return bpc;
 }
 
+extern "C" int pm_attn_workers_cfg(int hd, int cfg);
 // Warps of a full attention launch (the `workers` of pm_attn_work_list).
-extern "C" int pm_attn_workers(int hd) {
-  if (hd == 128) return attn_workers<128>();
-  if (hd == 64) return attn_workers<64>();
+extern "C" int pm_attn_workers(int hd) { return pm_attn_workers_cfg(hd, -1); }
+
+// ... of launch configuration `cfg` (0: 6 warps x 4 stages, 1: 12 x 2, 2: 8 x 3,
+// 3: 4 x 2 at 2 CTAs/SM; -1: the default / PM_ATTN_CFG).
+extern "C" int pm_attn_workers_cfg(int hd, int cfg) {
+  if (hd == 128) return attn_workers<128>(cfg);
+  if (hd == 64) return attn_workers<64>(cfg);
   return 0;
 }
 

@@ -293,10 +293,14 @@ def attn_blocks_per_chunk() -> int:
 class AttnWorkspace:
     """Chunk partials [M][Hkv][chunks][8][hd] + (m, l), merge counters and the work list."""
 
-    def __init__(self, m_cap, Hkv, hd, max_blocks, device):
+    def __init__(self, m_cap, Hkv, hd, max_blocks, device, cfg=None):
         self.bpc = attn_blocks_per_chunk()
         self.Hkv = Hkv
-        self.workers = attn_workers(hd) if torch.cuda.is_available() else 0
+        cuda = torch.cuda.is_available()
+        if cfg is None:
+            cfg = choose_attn_cfg(m_cap, Hkv, hd, max_blocks, self.bpc) if cuda else -1
+        self.cfg = cfg
+        self.workers = _C.lib().pm_attn_workers_cfg(hd, cfg) if cuda else 0
         self.max_chunks = max(1, -(-max_blocks // self.bpc))
         self.o = torch.empty(m_cap * Hkv * self.max_chunks * 8 * hd, dtype=torch.float32, device=device)
         self.ml = torch.empty(m_cap * Hkv * self.max_chunks * 16, dtype=torch.float32, device=device)
@@ -349,13 +353,50 @@ def attn_workers(hd: int) -> int:
     return _C.lib().pm_attn_workers(hd)
 
 
+# (cfg, KV-ring stages per warp) of the candidate launch configurations: both
+# keep 24 stage slots per SM, so a warp's streaming rate scales with its stages;
+# on a tie the deeper ring wins (measured on C3)
+ATTN_CFGS = ((2, 3), (1, 2))
+
+
+def choose_attn_cfg(m_cap: int, hkv: int, hd: int, max_blocks: int, bpc: int) -> int:
+    """Launch configuration of a workspace's attention kernel: the candidate
+    whose busiest warp finishes first when every row holds ``max_blocks``
+    blocks, under the work list's own size-sorted snake assignment (cost =
+    blocks of the busiest warp / its ring stages; ties go to the deeper ring).  Measured: Qwen3-32B
+    stage C3 (64 rows) 2.13 -> 2.06 ms/step with 8 x 3; C2 and C4 keep 12 x 2.
+    PM_ATTN_CFG forces one.  The choice never changes results."""
+    import os
+    if os.environ.get("PM_ATTN_CFG"):
+        return int(os.environ["PM_ATTN_CFG"])
+    import numpy as np
+    best, best_cost = -1, None
+    seq = np.full(m_cap, max_blocks * 16 - 1, dtype=np.int64)
+    nb = (seq + 15) // 16
+    for cfg, stages in ATTN_CFGS:
+        w = _C.lib().pm_attn_workers_cfg(hd, cfg)
+        if w <= 0:
+            continue
+        lst = attn_work_list(seq, bpc, hkv, w)
+        n = int(lst[0])
+        ent = lst[2:2 + 2 * n:2]
+        c_idx, r_idx = ent >> 16, ent & 0xffff
+        size = np.minimum(bpc, nb[r_idx] - c_idx * bpc)
+        items = np.repeat(size, hkv)                      # entry j -> items j*hkv .. j*hkv+hkv-1
+        load = np.bincount(np.arange(len(items)) % w, weights=items, minlength=w)
+        cost = load.max() / stages
+        if best_cost is None or cost < best_cost:
+            best, best_cost = cfg, cost
+    return best
+
+
 def paged_attention(tmap_kv, q, block_table, seq_lens, out, ws: AttnWorkspace, M, H, Hkv, hd, layer,
                     L_s, stream=None, kv_tokens=0):
     """``kv_tokens`` (sum of seq_lens, host-known) only feeds the optional timer."""
     def go():
         _C.call("pm_paged_attention", tmap_kv.ptr, _ptr(q), _ptr(block_table), _ptr(seq_lens), _ptr(ws.work), _ptr(out),
                 _ptr(ws.o), _ptr(ws.ml), _ptr(ws.counters), M, H, Hkv, hd, layer, L_s, block_table.shape[1],
-                ws.max_chunks, ws.bpc, _stream(stream))
+                ws.max_chunks, ws.bpc, ws.cfg, _stream(stream))
     if TIMER is None:
         go()
     else:
