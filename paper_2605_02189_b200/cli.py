@@ -55,8 +55,8 @@ def cmd_decode(args) -> int:
     kw = {}
     if args.prefill:
         kw.update(kv_init="prefill", prompts=_prompts(spec, reqs, args.seed))
-    trace, metrics = run_decode(state, cfg, params, spec, None, args.horizon, requests=reqs, seed=args.seed,
-                                pp=args.pp, **kw)
+    trace, metrics = run_decode(state, cfg, params, None, args.horizon, requests=reqs, seed=args.seed,
+                                model=spec, pp=args.pp, **kw)
     trace.to_jsonl(args.trace)
     record = metrics.to_record("dynamic", args.seed)
     with open(args.metrics, "w") as fh:

@@ -1,7 +1,7 @@
 """The B200 decode engine: the reference's ``simulate_decode`` driver shape
 over real hardware.
 
-``run_decode(state, cfg, params, spec, requests=..., horizon=...)`` mirrors
+``run_decode(state, cfg, params, noise_spec, horizon, *, requests, ...)`` mirrors
 ``pipemax.pipeline_sim.simulate_decode`` (REF pkg/src/pipemax/
 pipeline_sim.py:546-581) and returns ``(EventTrace, EpisodeMetrics)``; the
 loop body is the reference's ``_DecodeEngine.run`` (:386-543) with the
@@ -81,7 +81,8 @@ class DecodeEngine:
                  requests: dict, *, pp: int = 1, device="cuda", mode="dynamic", quota_tokens=0,
                  seed: int = 0, m_cap: int = None, timing=True, kv_init="random", prompts=None,
                  record_logits=False, max_pos=None, trace: EventTrace = None, graphs: bool = True,
-                 local_stages=None, staging_pool_requests: int = 2, lanes: int = None):
+                 local_stages=None, staging_pool_requests: int = 2, lanes: int = None,
+                 copy_priority: bool = True):
         """``local_stages``: which of the ``pp`` stages this process hosts
         (default all; one rank per stage under torchrun, see pipeline.py)."""
         self.spec, self.cfg, self.params = spec, cfg, params
@@ -119,7 +120,8 @@ class DecodeEngine:
             if record_logits:
                 ex.enable_logits()
             rep = HostReplica(len(rids), self.max_blocks, ex.block_bytes)
-            self.stages.append((ex, KvEngine(ex, rep, self.slot_of, self.dev, timing=timing)))
+            self.stages.append((ex, KvEngine(ex, rep, self.slot_of, self.dev, timing=timing,
+                                             low_priority_copies=copy_priority)))
         self.work_len = self.stages[0][0].aws.work_len
         self.bpc = self.stages[0][0].aws.bpc
         self.attn_hkv, self.attn_workers = self.stages[0][0].aws.Hkv, self.stages[0][0].aws.workers
@@ -323,7 +325,8 @@ class DecodeEngine:
         info = {"plan": work.plan, "batch_tokens": work.batch_tokens, "completed": list(work.completed),
                 "resident_tokens": self.control.resident_tokens, "capacity_tokens": self.control.capacity_tokens}
         for ex, kv in stages:
-            rec = {"t": t, "M": M, "info": info, "stream": kv.streams[lane], "serialize": self.serialize_lanes}
+            rec = {"t": t, "M": M, "info": info, "stream": kv.streams[lane], "lane": lane,
+                   "serialize": self.serialize_lanes}
             kv.prefetch(t, work, rec)
             recs.append(rec)
         self._upload_meta(work.rows, work.positions, work.tables, lane=lane)
@@ -407,14 +410,54 @@ class DecodeEngine:
         return m.finalize()
 
 
-def run_decode(state: SchedulerState, cfg: ClusterConfig, params: EstimatorParams, spec: ModelSpec,
-               noise_spec=None, horizon: int = None, *, requests: dict, seed: int = 0, pp: int = 1,
-               device="cuda", kv_init="random", prompts=None, **kw):
-    """Drop-in for ``simulate_decode`` (REF pipeline_sim.py:546-581) on B200:
-    same positional/keyword shape plus the model spec; ``noise_spec`` is
-    accepted and ignored (durations are measured).  Returns (trace, metrics)."""
+def _default_model(cfg: ClusterConfig) -> ModelSpec:
+    """The model a reference-style call (no ``model=``) runs: the BASELINE
+    shape whose whole-model KV bytes/token equals ``cfg.kv_bytes_per_token``,
+    else the tiny C1 model (the planner's arithmetic -- capacity_blocks,
+    budgets -- always comes from ``cfg`` itself)."""
+    from .models import SPECS, TINY
+    for spec in SPECS.values():
+        if spec.kv_bytes_per_token() == cfg.kv_bytes_per_token:
+            return spec
+    return TINY
+
+
+def run_decode(state: SchedulerState, cfg: ClusterConfig, params: EstimatorParams, noise_spec=None,
+               horizon: int = None, *, requests: dict, seed: int = 0, actual_params=None,
+               priority_enabled: bool = True, model=None, pp: int = 1, device="cuda", kv_init="random",
+               prompts=None, **kw):
+    """Drop-in for ``simulate_decode`` (REF pipeline_sim.py:546-549): the same
+    positional order ``(state, cfg, params, noise_spec, horizon)`` and
+    keywords ``requests, seed, actual_params, priority_enabled``; returns
+    ``(EventTrace, EpisodeMetrics)``.
+
+    * ``noise_spec`` / ``actual_params`` shape the reference's SIMULATED stage
+      duration (``estimate_decode_time(actual_params) x noise``, REF :423-427);
+      here durations are measured on the GPU, so both are accepted and unused.
+    * ``priority_enabled`` (REF ChannelSim two-lane priority, transfer.py:
+      195-213): True puts the KV copy streams at low stream priority under the
+      compute streams; False gives them default priority (the orchestration-
+      free baseline).
+    * B200 extras (keyword-only): ``model`` -- a ModelSpec or name (default
+      ``_default_model(cfg)``), ``pp`` stages in this process, ``kv_init``
+      ("random" | "prefill" with ``prompts``), and DecodeEngine options.
+    Raises ``ConfigError`` for a non-ClusterConfig ``cfg`` (REF :551-552)."""
+    from .models import SPECS
+    from .trace import ConfigError
+    if not isinstance(cfg, ClusterConfig):
+        raise ConfigError("cfg must be a ClusterConfig")
+    if model is None:
+        spec = _default_model(cfg)
+    elif isinstance(model, str):
+        if model not in SPECS:
+            raise ConfigError(f"unknown model {model!r} (one of {sorted(SPECS)})")
+        spec = SPECS[model]
+    elif isinstance(model, ModelSpec):
+        spec = model
+    else:
+        raise ConfigError(f"model must be a ModelSpec or a name, not {type(model).__name__}")
     eng = DecodeEngine(spec, state, cfg, params, requests, pp=pp, device=device, seed=seed,
-                       kv_init=kv_init, prompts=prompts, **kw)
+                       kv_init=kv_init, prompts=prompts, copy_priority=priority_enabled, **kw)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     start.record()

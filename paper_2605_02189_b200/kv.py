@@ -63,11 +63,16 @@ class HostReplica:
 class KvEngine:
     """Copy streams, events and the dependency rules of one stage."""
 
-    def __init__(self, executor, replica: HostReplica, slot_of: dict, device, timing: bool = True):
+    def __init__(self, executor, replica: HostReplica, slot_of: dict, device, timing: bool = True,
+                 low_priority_copies: bool = True):
+        """``low_priority_copies``: compute streams above the KV copy streams
+        (REF ChannelSim ``priority_enabled``: two priority lanes); False puts
+        every stream at the same (lowest) priority -- one FIFO lane."""
         self.ex, self.rep, self.slot_of = executor, replica, slot_of
         self.dev = device
         lo, hi = torch.cuda.Stream.priority_range()
-        self.compute = torch.cuda.Stream(device=device, priority=hi)
+        self._compute_prio = hi if low_priority_copies else lo
+        self.compute = torch.cuda.Stream(device=device, priority=self._compute_prio)
         self.streams = [self.compute]   # one compute stream per lane (micro-batch in flight)
         self.h2d = torch.cuda.Stream(device=device, priority=lo)
         self.d2h = torch.cuda.Stream(device=device, priority=lo)
@@ -83,10 +88,13 @@ class KvEngine:
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self.block_last_d2h = np.full(executor.pool_blocks, -1, dtype=np.int64)
-        # last step whose compute read or wrote each block: with several lanes
-        # (micro-batches in flight on different streams) a block freed by one
-        # step and reused by the next needs an explicit compute -> compute edge
-        self.block_last_compute = np.full(executor.pool_blocks, -1, dtype=np.int64)
+        # per lane: the last step of that lane whose compute read or wrote each
+        # block.  With several lanes (micro-batches in flight on different
+        # streams) a block freed by one step and reused by a later one needs an
+        # explicit compute -> compute edge to the newest toucher on EVERY other
+        # lane (same-lane order is stream order); one array per lane so an
+        # older toucher on lane B is not masked by a newer one on lane A.
+        self.block_last_compute = [np.full(executor.pool_blocks, -1, dtype=np.int64)]
 
     def reset_phase(self):
         """New decode phase (episode.py): step numbers restart at 0, so the
@@ -97,7 +105,8 @@ class KvEngine:
         self.compute_done.clear()
         self.h2d_done.clear()
         self.block_last_d2h[:] = -1
-        self.block_last_compute[:] = -1
+        for a in self.block_last_compute:
+            a[:] = -1
 
     def load_resident(self, tables: dict):
         """Bulk H2D of resident requests' KV (host replica -> their blocks)
@@ -119,9 +128,20 @@ class KvEngine:
         return len(dst) * bb
 
     def add_lane(self) -> int:
-        lo, hi = torch.cuda.Stream.priority_range()
-        self.streams.append(torch.cuda.Stream(device=self.dev, priority=hi))
+        self.streams.append(torch.cuda.Stream(device=self.dev, priority=self._compute_prio))
+        self.block_last_compute.append(np.full(self.ex.pool_blocks, -1, dtype=np.int64))
         return len(self.streams) - 1
+
+    def _wait_touchers(self, stream, blocks, skip_lane=None, skip_step=None):
+        """``stream`` waits for the newest compute step of every lane (except
+        ``skip_lane``, ordered by stream order) that touched ``blocks``."""
+        for li, arr in enumerate(self.block_last_compute):
+            if li == skip_lane:
+                continue
+            dep = int(arr[blocks].max())
+            ev = self.compute_done.get(dep)
+            if ev is not None and dep != skip_step:
+                stream.wait_event(ev)
 
     def _event(self):
         return torch.cuda.Event(enable_timing=self.timing)
@@ -142,10 +162,8 @@ class KvEngine:
                 src.append(base + lb * bb)
                 targets.add(pb)
         s = self.h2d
-        last_c = int(self.block_last_compute[list(targets)].max())
-        prev = self.compute_done.get(last_c)
-        if prev is not None:
-            s.wait_event(prev)            # the reused blocks' last reader (normally step t-1)
+        # the reused blocks' last readers on every lane (normally step t-1)
+        self._wait_touchers(s, np.fromiter(targets, dtype=np.int64))
         # the host copy must hold the requests' last token, and no offload may
         # still be reading a block this copy overwrites
         dep = max((self.last_write.get(rid, -1) for rid, _, _ in work.prefetch), default=-1)
@@ -186,11 +204,9 @@ class KvEngine:
         # blocks this step touches that another lane's step touched last
         used = rec.get("used_blocks")
         if used is not None and len(used):
-            dep = int(self.block_last_compute[used].max())
-            ev = self.compute_done.get(dep)
-            if ev is not None and dep != t:
-                s.wait_event(ev)
-            self.block_last_compute[used] = t
+            lane = rec.get("lane", 0)
+            self._wait_touchers(s, used, skip_lane=lane, skip_step=t)
+            self.block_last_compute[lane][used] = t
         # a growth block handed out this step may still be read by an offload
         grow = [work.tables[r][p // 16] for r, p in zip(work.rows, work.positions) if p % 16 == 0]
         if grow:
