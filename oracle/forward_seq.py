@@ -125,17 +125,18 @@ class SeqModel:
 
     # ------------------------------------------------------------------ API
     @torch.no_grad()
-    def teacher_forced(self, seqs, want):
+    def teacher_forced(self, seqs, want, numpy=True):
         """seqs[j]: token ids of request j (prompt + fed decode tokens);
         want[j]: positions whose logits to return.  Returns a list of fp32
-        numpy arrays [len(want[j]), V] -- the logits of the NEXT token after
-        each wanted position (what the engine emits when it decodes it)."""
+        arrays [len(want[j]), V] (numpy, or device tensors with
+        ``numpy=False``) -- the logits of the NEXT token after each wanted
+        position (what the engine emits when it decodes it)."""
         out = [None] * len(seqs)
         for grp in self._groups([len(s) for s in seqs]):
             caches = [[(None, None)] * len(self.layers) for _ in grp]
             res = self._run([seqs[j] for j in grp], caches, [want[j] for j in grp])
             for j, r in zip(grp, res):
-                out[j] = r.cpu().numpy()
+                out[j] = r.cpu().numpy() if numpy else r
         return out
 
     @torch.no_grad()

@@ -143,7 +143,7 @@ class DecodeEngine:
             for _, kv in self.stages:
                 assert kv.add_lane() == li
         self.record_logits = record_logits
-        self.logits_log = []   # (t, rows, positions, logits[M, V] np) when recording
+        self.logits_log = []   # (t, rows, positions, logits[M, V]) when recording (np, or torch if "device")
         self.ids_log = []      # (t, rows, ids np)
         self.t = 0
         self.n_evicted = self.n_prefetched = 0
@@ -340,7 +340,10 @@ class DecodeEngine:
         if self.record_logits and M:
             last = stages[-1][0]
             torch.cuda.synchronize()
-            self.logits_log.append((t, list(work.rows), list(work.positions), last.logits[:M].cpu().numpy()))
+            if self.record_logits == "device":   # keep on the GPU (real-shape parity tests)
+                self.logits_log.append((t, list(work.rows), list(work.positions), last.logits[:M].clone()))
+            else:
+                self.logits_log.append((t, list(work.rows), list(work.positions), last.logits[:M].cpu().numpy()))
             self.ids_log.append((t, list(work.rows), last.out_ids[:M].cpu().numpy().copy()))
         self.t += 1
         return work
