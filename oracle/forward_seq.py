@@ -36,7 +36,14 @@ class SeqModel:
     k_norm); embed [V, d]; final_norm [d]; lm_head [V, d]; rope_tab
     [max_pos, hd] (cos | sin halves, models.rope_table)."""
 
-    def __init__(self, hp, layers, embed, final_norm, lm_head, rope_tab, device="cpu", chunk_tokens=8192):
+    def __init__(self, hp, layers, embed, final_norm, lm_head, rope_tab, device="cpu", chunk_tokens=8192,
+                 storage_bf16=False):
+        """storage_bf16: also round to bf16 wherever the GPU path STORES a
+        bf16 tensor (as ``forward_ref.RefModel(storage_bf16=True)``: norm
+        outputs, q/k/v, cached K/V, attention output, SwiGLU activation) --
+        the twin that separates kernel arithmetic from bf16 storage error.
+        The default is the pure fp32 reference."""
+        self.r = (lambda t: t.to(torch.bfloat16).to(torch.float32)) if storage_bf16 else (lambda t: t)
         torch.backends.cuda.matmul.allow_tf32 = False
         torch.backends.cudnn.allow_tf32 = False
         self.hp, self.dev = hp, torch.device(device)
@@ -62,15 +69,15 @@ class SeqModel:
         = (K, V) [P, Hkv, hd] of request j's earlier positions (appended to)."""
         hp, w = self.hp, self.layers[li]
         H, Hkv, hd, eps = hp["H"], hp["Hkv"], hp["hd"], hp["eps"]
-        T = x.shape[0]
-        h = _rmsnorm(x, w["attn_norm"], eps)
-        q = (h @ w["wq"].T).view(T, H, hd)
-        k = (h @ w["wk"].T).view(T, Hkv, hd)
-        v = (h @ w["wv"].T).view(T, Hkv, hd)
+        T, R = x.shape[0], self.r
+        h = R(_rmsnorm(x, w["attn_norm"], eps))
+        q = R(h @ w["wq"].T).view(T, H, hd)
+        k = R(h @ w["wk"].T).view(T, Hkv, hd)
+        v = R(h @ w["wv"].T).view(T, Hkv, hd)
         if hp["qk_norm"]:
             q = _rmsnorm(q, w["q_norm"], eps)
             k = _rmsnorm(k, w["k_norm"], eps)
-        q, k = self._rope(q, pos), self._rope(k, pos)
+        q, k = R(self._rope(q, pos)), R(self._rope(k, pos))
         o = torch.empty(T, H, hd, device=self.dev)
         g = H // Hkv
         scale = 1.0 / float(np.sqrt(hd))
@@ -86,9 +93,9 @@ class SeqModel:
             qpos = torch.arange(L - n, L, device=self.dev)[:, None]
             s = s.masked_fill(torch.arange(L, device=self.dev)[None, :] > qpos, float("-inf"))
             o[a:b] = (torch.softmax(s, dim=-1) @ Vh).permute(1, 0, 2)
-        x = x + o.reshape(T, H * hd) @ w["wo"].T
-        h = _rmsnorm(x, w["mlp_norm"], eps)
-        return x + (torch.nn.functional.silu(h @ w["w_gate"].T) * (h @ w["w_up"].T)) @ w["w_down"].T
+        x = x + R(o).reshape(T, H * hd) @ w["wo"].T
+        h = R(_rmsnorm(x, w["mlp_norm"], eps))
+        return x + R(torch.nn.functional.silu(h @ w["w_gate"].T) * (h @ w["w_up"].T)) @ w["w_down"].T
 
     def _run(self, new_tokens, caches, want):
         """Run every request's ``new_tokens[j]`` after its cache; returns, per
@@ -108,7 +115,7 @@ class SeqModel:
         out = []
         for j, (a, b) in enumerate(segs):
             sel = x[a:b][torch.as_tensor(want[j], device=self.dev, dtype=torch.long)]
-            out.append(_rmsnorm(sel, self.final_norm, self.hp["eps"]) @ self.lm_head.T)
+            out.append(self.r(_rmsnorm(sel, self.final_norm, self.hp["eps"])) @ self.lm_head.T)
         return out
 
     def _groups(self, lengths):
