@@ -206,6 +206,26 @@ class StageExecutor:
         return n
 
     # ------------------------------------------------------------------ roofline
+    def gemm_bytes(self, M: int) -> int:
+        """Algorithmic bytes of one step's projection GEMMs (bench.py's kernel
+        roofline): each weight once, the bf16 activations in, the outputs
+        (bf16; fp32 residual read + write and the normalised bf16 copy for
+        O/down; logits fp32 when kept)."""
+        tot = 0
+        for w in self.W:
+            for key, out_b in (("qkv", 2), ("o", 0), ("gu", 1), ("down", 0)):
+                lin = w[key]
+                tot += lin.weight_bytes + M * lin.k * 2 + (M * lin.n_out * out_b if out_b else M * lin.n_out * 10)
+        if self.last:
+            tot += self.lm_head.weight_bytes + M * self.lm_head.k * 2 + (M * self.spec.vocab * 4 if self.logits is not None else 0)
+        return tot
+
+    def attn_bytes(self, kv_tokens: int, M: int = 0) -> int:
+        """Algorithmic bytes of one step's attention launches: every row's KV
+        (``kv_tokens`` = sum of sequence lengths) once per layer, q in, o out."""
+        s = self.spec
+        return self.L_s * (kv_tokens * 2 * s.Hkv * s.hd * 2 + 2 * M * s.H * s.hd * 2)
+
     def step_bytes(self, M: int, kv_tokens: int) -> int:
         """Algorithmic HBM bytes of one step: weights once, the micro-batch's
         KV once per layer, new KV written once, activations (stated, small)."""
