@@ -384,7 +384,7 @@ def measure_e2e(eng, steps, dist=None):
                     "one step later; H2D = KV prefetch + step metadata, D2H = KV offload + ids"}
 
 
-KIND_OF = (("gemm_stream_kernel", "gemm"), ("paged_attn_kernel", "attention"),
+KIND_OF = (("gemm_stream_kernel", "gemm"), ("gemm_cluster_kernel", "gemm"), ("paged_attn_kernel", "attention"),
            ("gemm_", "gemm_fixup"), ("rmsnorm", "norm"), ("embed", "embed"), ("argmax", "argmax"),
            ("meta_upload", "meta"))
 

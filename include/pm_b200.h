@@ -106,6 +106,32 @@ int pm_prepare_attention(void);
 int pm_argmax_reduce(const float* val, const int* idx, int n_tiles, int M, int m_cap, int* out_ids,
                      int* tok_table, const int* slots, void* stream);
 
+/* ---- cluster split-K projection (gemm_cl.cu): split-K reduction and epilogue in ONE kernel ----------
+ * cluster = 2 * slices CTAs (pair = the two 128-row halves of a 256-row unit, sharing a multicast
+ * activation tile; slices split K); n_clusters clusters own consecutive units; the slices' fp32 partials
+ * are summed in slice order (L2 scratch, cluster-scope mbarrier hand-off).  m_tok <= bn <= 128; tmap_x box
+ * [bn/2 rows x 64].  epilogue: 0 bf16 store, 1 SiLU(gate)*up (interleaved rows), 2 resid += acc (fp32;
+ * with norm_w: xn = bf16(resid * norm_w) and ssq_out[n_out/128][m_cap] = per-128-row sums of resid^2),
+ * 3 logits (out may be NULL) + argmax tiles, 4 bf16 round + q/k norm + RoPE + q_out / paged KV append.
+ * ssq_in (NULL = none): the input rows are bf16(x * w) of a folded RMSNorm; every token column is scaled
+ * by rsqrt(sum_t ssq_in[t][m] / d_in + eps).  Replaces pm_gemm / pm_gemm_resid_rmsnorm /
+ * pm_gemm_qkv_rope and their fixup kernels for m_tok <= 128. */
+int pm_gemm_cl(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok, int bn,
+               int m_cap, int slices, int n_clusters, int epilogue, void* out, int ld_out, const float* ssq_in,
+               int n_ht_in, int d_in, float eps, float* resid, const void* norm_w, void* xn, float* ssq_out,
+               float* amax_val, int* amax_idx, void* q_out, void* pool, const int* block_table,
+               const int* positions, const float* rope, const void* qn_w, const void* kn_w, int H, int Hkv, int hd,
+               int layer, int L_s, int max_blocks, float* part, void* stream);
+/* part: fp32 scratch, n_clusters * 2 * slices * bn * 128 floats (split-K partials, L2-resident) */
+/* co-resident clusters of `cluster_size` CTAs of the bn instantiation (cudaOccupancyMaxActiveClusters) */
+int pm_gemm_cl_max_clusters(int bn, int cluster_size, int* out);
+/* profiling only: per-CTA globaltimer stamps of the last launch under PM_CL_TRACE=1 ([160][8] u64) */
+int pm_gemm_cl_trace_read(void* dst);
+/* weight-ring stages of the bn instantiation */
+int pm_gemm_cl_stages(int bn);
+/* one-time kernel attributes of the cluster GEMM */
+int pm_prepare_gemm_cl(void);
+
 #ifdef __cplusplus
 }
 #endif

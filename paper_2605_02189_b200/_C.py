@@ -43,6 +43,12 @@ _SIGS = {
     "pm_attn_blocks_per_split": [],
     "pm_prepare_gemm": [],
     "pm_prepare_attention": [],
+    "pm_gemm_cl": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _I, _F, _P, _P, _P, _P, _P, _P,
+                   _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P],
+    "pm_gemm_cl_max_clusters": [_I, _I, C.POINTER(_I)],
+    "pm_gemm_cl_stages": [_I],
+    "pm_gemm_cl_trace_read": [_P],
+    "pm_prepare_gemm_cl": [],
 }
 
 _lib = None

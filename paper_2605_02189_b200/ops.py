@@ -155,6 +155,95 @@ def gemm_plan(n_units: int, kb: int, m_tok: int, sms: int = None):
     return bn, per * workers, segs, tt, pair
 
 
+# ---------------------------------------------------------------- cluster split-K GEMM (gemm_cl.cu)
+import os as _os
+
+# The cluster path finishes every projection (split-K reduction + epilogue)
+# inside one kernel; with PM_GEMM_CL=1 steps of up to CL_MAX_M rows use it.
+# Default OFF: measured slower than stream-K + fixup at C2 (QKV 27.9 vs 16.4
+# us, tools/gemm_cl_bench.py): each CTA's weight stream tops out near 42 GB/s
+# when a 128-row half shares SM ingress with a full activation tile, and the
+# owner-phase reduction is latency-bound (profiles/r2/gemm_cl_*.txt).
+CL_GEMM = _os.environ.get("PM_GEMM_CL", "0") == "1"
+CL_MAX_M = 128
+CL_EPI_STORE, CL_EPI_SILU, CL_EPI_RESID, CL_EPI_LOGITS, CL_EPI_QKV_ROPE = 0, 1, 2, 3, 4
+# CTAs a cluster launch may span, and the per-SM weight-streaming rate the
+# planner assumes (bytes/s); tuning knobs
+CL_CTAS = int(_os.environ.get("PM_CL_CTAS", "148"))
+CL_SM_BPS = float(_os.environ.get("PM_CL_SM_GBPS", "60")) * 1e9
+CL_HBM_BPS = 6.5e12
+CL_UNIT_S = 0.6e-6          # per-unit reduction/epilogue latency not hidden behind the next unit
+_CL_MAX_ACTIVE_FALLBACK = {2: 74, 4: 33, 6: 22, 8: 15}   # measured on B200 (no GPU: planner tests)
+_cl_active = {}
+
+
+def cl_max_clusters(cluster_size: int) -> int:
+    """Co-resident clusters of ``cluster_size`` CTAs (the 128-token
+    instantiation, the largest shared-memory footprint)."""
+    v = _cl_active.get(cluster_size)
+    if v is None:
+        if torch.cuda.is_available():
+            _C.call("pm_prepare_gemm_cl")   # the smem attribute the occupancy query depends on
+            out = C.c_int(0)
+            _C.call("pm_gemm_cl_max_clusters", 128, cluster_size, C.byref(out))
+            v = int(out.value)
+        else:
+            v = _CL_MAX_ACTIVE_FALLBACK[cluster_size]
+        _cl_active[cluster_size] = v
+    return v
+
+
+def cl_plan(n_units: int, kb: int, ctas: int = None):
+    """(slices S, clusters NC) of a cluster split-K launch: the choice that
+    minimises the modelled time max(busiest CTA's weight bytes / per-SM rate,
+    all weight bytes / HBM rate) + per-unit reduction latency, over S in 1..4
+    and NC co-resident clusters of 2S CTAs.  Depends on (units, K) only --
+    never on the token count -- so results are batch-invariant."""
+    ctas = CL_CTAS if ctas is None else ctas
+    best, best_t = None, None
+    total = n_units * kb * 2 * CL_BK_BYTES
+    for S in (1, 2, 3, 4):
+        if S > kb:
+            continue
+        cs = 2 * S
+        nc_max = min(n_units, cl_max_clusters(cs), ctas // cs)
+        for nc in range(1, nc_max + 1):
+            units = -(-n_units // nc)
+            per_cta = units * -(-kb // S) * CL_BK_BYTES
+            t = max(per_cta / CL_SM_BPS, total / CL_HBM_BPS) + units * CL_UNIT_S
+            key = (round(t * 1e8), nc * cs)
+            if best_t is None or key < best_t:
+                best, best_t = (S, nc), key
+    if best is None:
+        raise RuntimeError(f"no co-resident cluster plan for {n_units} units x {kb} k-blocks")
+    return best
+
+
+CL_BK_BYTES = 128 * BK * 2   # one 128x64 bf16 weight tile
+_cl_part = {}
+_cl_prepared = False
+
+
+def cl_scratch(device) -> torch.Tensor:
+    """fp32 split-K partial scratch of the cluster GEMM: one [128 x 128]
+    slot per CTA of the largest launch.  Shared by every launch on the device:
+    each kernel writes its slots only after its programmatic-launch wait, i.e.
+    after the previous kernel on its stream finished; kernels of different
+    streams (lanes) get their own via ``cl_scratch_for``."""
+    return cl_scratch_for(device, 0)
+
+
+def cl_scratch_for(device, lane: int) -> torch.Tensor:
+    key = (str(device), lane)
+    t = _cl_part.get(key)
+    if t is None:
+        t = _cl_part[key] = torch.empty(CL_CTAS_MAX * 128 * 128, dtype=torch.float32, device=device)
+    return t
+
+
+CL_CTAS_MAX = 160
+
+
 class GemmWorkspace:
     """Stream-K partials, per-row counters and argmax partials shared by all
     projections of one executor (launches on one stream run in order)."""
@@ -189,6 +278,8 @@ class Linear:
         self.weight_bytes = self.n_out * self.k * 2
         self._plans = {}
         self.sms = None   # SMs the stream-K workers span (None: GEMM_CTAS)
+        self._cl = None   # (slices, clusters) of the cluster split-K launch (cl_plan)
+        self.cl_ctas = None
 
     def launches(self, m_tok) -> int:
         """Kernels one call launches: the stream-K GEMM, plus gemm_reduce when
@@ -238,6 +329,37 @@ class Linear:
                     m_tok, bn, grid, int(pair), _ptr(resid), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, _ptr(norm_w),
                     _ptr(xn), float(eps), _ptr(ws.row_cnt), int(split_norm), _stream(stream))
         self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * (8 + 4 + 2), stream, go)
+
+    def cl(self, x_maps: dict, m_tok: int, epilogue: int, stream=None, *, m_cap: int, out=None, ld_out=0, rs=None, eps=0.0,
+           resid=None, norm_w=None, xn=None, ssq_out=None, ws: GemmWorkspace = None, rope=None, part=None):
+        """Cluster split-K launch (pm_gemm_cl): the whole projection incl. its
+        epilogue in one kernel.  ``rs`` = (ssq tensor, d_in): the input rows
+        are bf16(x * w) of a folded RMSNorm (scale every token column by
+        rsqrt(mean(x^2) + eps)); ``rope`` = dict(q_out, pool, block_table,
+        positions, rope, qn_w, kn_w, H, Hkv, hd, layer, L_s) for the QKV
+        epilogue; LOGITS writes the argmax tiles of ``ws``.  ``m_cap``: the row
+        capacity of the activation / ssq / argmax buffers (their row stride).
+        ``part``: the split-K partial scratch (cl_scratch_for; one per stream
+        that may run GEMMs concurrently)."""
+        assert m_tok <= CL_MAX_M
+        bn = bn_for(m_tok)
+        global _cl_prepared
+        if not _cl_prepared:
+            _C.call("pm_prepare_gemm_cl")
+            _cl_prepared = True
+        if self._cl is None:
+            self._cl = cl_plan(self.n_units, self.kb, self.cl_ctas)
+        S, nc = self._cl
+        ssq_in, n_ht, d_in = (None, 0, 0) if rs is None else (rs[0], rs[1] // 128, rs[1])
+        r = rope or {}
+        amax_v, amax_i = (ws.amax_val, ws.amax_idx) if epilogue == CL_EPI_LOGITS else (None, None)
+        _C.call("pm_gemm_cl", _ptr(self.packed), x_maps[bn // 2].ptr, self.n_out, self.n_units, self.k, m_tok, bn,
+                m_cap, S, nc, epilogue, _ptr(out), ld_out, _ptr(ssq_in), n_ht, d_in, float(eps), _ptr(resid),
+                _ptr(norm_w), _ptr(xn), _ptr(ssq_out), _ptr(amax_v), _ptr(amax_i), _ptr(r.get("q_out")),
+                _ptr(r.get("pool")), _ptr(r.get("block_table")), _ptr(r.get("positions")), _ptr(r.get("rope")),
+                _ptr(r.get("qn_w")), _ptr(r.get("kn_w")), r.get("H", 0), r.get("Hkv", 0), r.get("hd", 0),
+                r.get("layer", 0), r.get("L_s", 0), r["block_table"].shape[1] if rope else 0, _ptr(part if part is not None else cl_scratch(self.packed.device)),
+                _stream(stream))
 
     def qkv_rope(self, x_maps: dict, m_tok: int, qkv, ws: GemmWorkspace, q_out, pool, block_table, positions,
                  rope, qn_w, kn_w, H, Hkv, hd, layer, L_s, eps, stream=None, prefetch=None):

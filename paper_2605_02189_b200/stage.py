@@ -74,6 +74,7 @@ class StageExecutor:
         # greedy-token table indexed by request slot -- shared by every lane
         self.tok_table = torch.zeros(n_slots, dtype=i32, device=device)
         _C.call("pm_prepare_gemm")
+        _C.call("pm_prepare_gemm_cl")
         _C.call("pm_prepare_attention")
         self._alloc_lane()
 
@@ -89,6 +90,12 @@ class StageExecutor:
         self.q = torch.zeros(m_cap, s.H, s.hd, dtype=b16, device=device)
         self.attn = torch.zeros(m_cap, s.H * s.hd, dtype=b16, device=device)
         self.act = torch.zeros(m_cap, s.ffn, dtype=b16, device=device)
+        # folded RMSNorm (cluster GEMM path): per-(128-feature tile, row) sums
+        # of squares of the residual, written by the O/down epilogues and read
+        # by the next projection's epilogue
+        self.ssq = torch.zeros(s.d // 128, m_cap, dtype=f32, device=device)
+        # split-K partial scratch of the cluster GEMMs (per lane: lanes run concurrently)
+        self.cl_part = torch.empty(ops.CL_CTAS_MAX * 128 * 128, dtype=f32, device=device)
         self.xn_maps = ops.activation_maps(self.xn)
         self.attn_maps = ops.activation_maps(self.attn)
         self.act_maps = ops.activation_maps(self.act)
@@ -138,6 +145,8 @@ class StageExecutor:
         s = self.spec
         if M == 0:
             return
+        if ops.CL_GEMM and M <= ops.CL_MAX_M:
+            return self._forward_cl(M, stream, prefill_tokens, layer_hook)
         if self.first:
             if prefill_tokens:   # prompt chunk: row m embeds prefill_tokens[m]
                 ops.embed(self.prefill_tokens, None, self.embed, self.resid, M, stream)
@@ -170,6 +179,44 @@ class StageExecutor:
             self.lm_head(self.xn_maps, M, ops.EPI_LOGITS_ARGMAX, self.logits, s.vocab, self.gws, stream)
             ops.argmax_reduce(self.gws, self.lm_head.n_units, M, self.out_ids, self.tok_table, self.slots, stream)
 
+    def _forward_cl(self, M: int, stream, prefill_tokens: bool, layer_hook):
+        """forward() on the cluster split-K GEMMs: every projection finishes
+        its split-K reduction and its epilogue inside its own kernel, and the
+        RMSNorm before gate/up, the next QKV and the lm_head is folded into
+        the producing O/down epilogue (xn = bf16(x * w) + sum-of-squares
+        partials) and the consuming GEMM's per-token scale.  5 launches per
+        layer: QKV(+q/k norm, RoPE, KV append), attention, O(+resid),
+        gate/up(+SiLU), down(+resid)."""
+        s = self.spec
+        if self.first:
+            if prefill_tokens:
+                ops.embed(self.prefill_tokens, None, self.embed, self.resid, M, stream)
+            else:
+                ops.embed(self.tok_table, self.slots, self.embed, self.resid, M, stream)
+        ops.rmsnorm(self.resid, self.W[0]["attn_norm"], self.xn, M, s.eps, stream)
+        rs = None   # the first QKV reads a normalised xn
+        for li, w in enumerate(self.W):
+            w["qkv"].cl(self.xn_maps, M, ops.CL_EPI_QKV_ROPE, stream, m_cap=self.m_cap, part=self.cl_part, rs=rs, eps=s.eps,
+                        rope=dict(q_out=self.q, pool=self.pool, block_table=self.block_table, positions=self.positions,
+                                  rope=self.rope, qn_w=w["q_norm"], kn_w=w["k_norm"], H=s.H, Hkv=s.Hkv, hd=s.hd,
+                                  layer=li, L_s=self.L_s))
+            if layer_hook is not None:
+                layer_hook(li)
+            ops.paged_attention(self.pool_map, self.q, self.block_table, self.seq_lens, self.attn, self.aws,
+                                M, s.H, s.Hkv, s.hd, li, self.L_s, stream)
+            w["o"].cl(self.attn_maps, M, ops.CL_EPI_RESID, stream, m_cap=self.m_cap, part=self.cl_part, resid=self.resid, norm_w=w["mlp_norm"],
+                      xn=self.xn, ssq_out=self.ssq)
+            w["gu"].cl(self.xn_maps, M, ops.CL_EPI_SILU, stream, m_cap=self.m_cap, part=self.cl_part, out=self.act, ld_out=s.ffn, rs=(self.ssq, s.d),
+                       eps=s.eps)
+            nxt = self.W[li + 1]["attn_norm"] if li + 1 < len(self.W) else (self.final_norm if self.last else None)
+            w["down"].cl(self.act_maps, M, ops.CL_EPI_RESID, stream, m_cap=self.m_cap, part=self.cl_part, resid=self.resid, norm_w=nxt,
+                         xn=self.xn if nxt is not None else None, ssq_out=self.ssq if nxt is not None else None)
+            rs = (self.ssq, s.d) if nxt is not None else None
+        if self.last:
+            self.lm_head.cl(self.xn_maps, M, ops.CL_EPI_LOGITS, stream, m_cap=self.m_cap, part=self.cl_part, out=self.logits, ld_out=s.vocab, rs=rs,
+                            eps=s.eps, ws=self.gws)
+            ops.argmax_reduce(self.gws, self.lm_head.n_units, M, self.out_ids, self.tok_table, self.slots, stream)
+
     def run(self, M: int, stream, graphs: bool = True, kv_tokens: int = 0):
         """forward(M) on ``stream``; with ``graphs`` the whole kernel sequence
         for this M is captured once into a CUDA graph and replayed (the step's
@@ -197,6 +244,8 @@ class StageExecutor:
         down projections (GEMM + reduce/residual/RMSNorm kernel each) and the
         gate/up GEMM (1-2 launches); lm_head (1-2) + argmax."""
         M = M or self.m_cap
+        if ops.CL_GEMM and M <= ops.CL_MAX_M:
+            return (1 if self.first else 0) + 1 + 5 * self.L_s + (2 if self.last else 0)
         n = (1 if self.first else 0) + 1 + self.L_s * (2 + 1 + 2 + 2)
         n += sum(w["gu"].launches(M) for w in self.W)
         if not self.last:
