@@ -48,7 +48,7 @@
 
 namespace {
 
-constexpr int CL_THREADS = 224;            // w0 weight producer, w1 MMA, w2..w5 epilogue, w6 X producer
+constexpr int CL_THREADS = 288;            // w0/w7 weight producers, w1 MMA, w2..w5 epilogue, w6/w8 X producers
 constexpr int CL_BK = 64;
 constexpr int CL_WBYTES = 128 * CL_BK * 2; // one 128x64 bf16 weight tile (16 KB)
 constexpr int CL_SMEM_MAX = 232448;        // opt-in dynamic smem per CTA (227 KB)
@@ -84,6 +84,8 @@ struct ClArgs {
   float* ssq_out;           // [n_out / 128][m_cap]
   float* part;              // [grid][BN][128] fp32 split-K partials (L2 scratch)
   int trace;                // profiling only: per-CTA %globaltimer stamps into g_cl_trace
+  int debug;                // profiling only (PM_CL_DEBUG): bit0 no activation loads, bit1 no multicast,
+                            // bit2 no MMA (wrong numerics)
   // LOGITS
   float* amax_val;          // [n_units * 2][m_cap]
   int* amax_idx;
@@ -335,12 +337,14 @@ __global__ void __launch_bounds__(CL_THREADS, 1) gemm_cluster_kernel(const __gri
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) CL_TRACE(1);
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 7) {
     if (lane == 0) {
-      // ---------------- weight producer: this half's 16 KB chunks, WS deep.  Weights do not
-      // depend on the previous kernel, so the ring fills before the dependency wait.
+      // ---------------- weight producers: this half's 16 KB chunks, WS deep, issued by two
+      // threads (even / odd chunks): one thread's bulk copies are served at ~3.6 M ops/s
+      // (tools/sm_stream_probe.cu).  Weights do not depend on the previous kernel, so the
+      // ring fills before the dependency wait.
       const uint64_t pol_w = policy_evict_first();
-      for (long long it = 0; it < total; ++it) {
+      for (long long it = warp == 0 ? 0 : 1; it < total; it += 2) {
         const int s = (int)(it % C::WS);
         if (it >= C::WS) mbar_wait(&wempty[s], (uint32_t)(((it / C::WS) - 1) & 1));
         mbar_arrive_expect_tx(&wfull[s], CL_WBYTES);
@@ -350,19 +354,28 @@ __global__ void __launch_bounds__(CL_THREADS, 1) gemm_cluster_kernel(const __gri
       }
     }
     __syncwarp();
-  } else if (warp == 6) {
-    // ---------------- activation producer: half of each [BN x 64] tile, multicast to the pair
+  } else if (warp == 6 || warp == 8) {
+    // ---------------- activation producers (even / odd steps): half of each [BN x 64] tile,
+    // multicast to the pair
     pdl_wait();
     if (lane == 0) {
       const uint64_t pol_x = policy_evict_last();
-      for (long long it = 0; it < total; ++it) {
+      for (long long it = warp == 6 ? 0 : 1; it < total; it += 2) {
         const int s = (int)(it % C::XS);
         // both CTAs of the pair released the stage (the multicast writes both)
         if (it >= C::XS) mbar_wait(&xempty[s], (uint32_t)(((it / C::XS) - 1) & 1));
-        mbar_arrive_expect_tx(&xfull[s], C::X_BYTES);
         const int kb = k0 + (int)(it % nk);
-        tma_load_2d_mc(sx + s * C::X_BYTES + half * (BN / 2) * 128, &tmap_x, &xfull[s], kb * CL_BK, half * (BN / 2),
-                       pair_mask, pol_x);
+        if (a.debug & 1) {
+          mbar_arrive(&xfull[s]);
+        } else if (a.debug & 2) {
+          mbar_arrive_expect_tx(&xfull[s], C::X_BYTES);
+          tma_load_2d(sx + s * C::X_BYTES, &tmap_x, &xfull[s], kb * CL_BK, 0, pol_x);
+          tma_load_2d(sx + s * C::X_BYTES + (BN / 2) * 128, &tmap_x, &xfull[s], kb * CL_BK, BN / 2, pol_x);
+        } else {
+          mbar_arrive_expect_tx(&xfull[s], C::X_BYTES);
+          tma_load_2d_mc(sx + s * C::X_BYTES + half * (BN / 2) * 128, &tmap_x, &xfull[s], kb * CL_BK,
+                         half * (BN / 2), pair_mask, pol_x);
+        }
       }
     }
     __syncwarp();
@@ -385,8 +398,11 @@ __global__ void __launch_bounds__(CL_THREADS, 1) gemm_cluster_kernel(const __gri
           tc_fence_after();
           const uint64_t da = umma_desc_sw128(smem_u32(sw + ws * CL_WBYTES));
           const uint64_t db = umma_desc_sw128(smem_u32(sx + xs * C::X_BYTES));
+          if (!(a.debug & 4)) {
 #pragma unroll
-          for (int k = 0; k < CL_BK / 16; ++k) tc_mma_bf16(acc, da + 2 * k, db + 2 * k, idesc, (kk > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < CL_BK / 16; ++k)
+              tc_mma_bf16(acc, da + 2 * k, db + 2 * k, idesc, (kk > 0 || k > 0) ? 1u : 0u);
+          }
           tc_commit(&wempty[ws]);
           tc_commit_mc(&xempty[xs], pair_mask);   // release the activation stage in both CTAs of the pair
         }
@@ -556,6 +572,9 @@ extern "C" int pm_gemm_cl(const void* w_packed, const void* tmap_x, int n_out, i
   a.part = part;
   static const int trace = getenv("PM_CL_TRACE") ? atoi(getenv("PM_CL_TRACE")) : 0;   // profiling only
   a.trace = trace;
+  static const int dbg = getenv("PM_CL_DEBUG") ? atoi(getenv("PM_CL_DEBUG")) : 0;   // profiling only
+  a.debug = dbg;
+
   a.ra = ClRope{reinterpret_cast<bf16*>(q_out), reinterpret_cast<bf16*>(pool), block_table, positions, rope,
                 reinterpret_cast<const bf16*>(qn_w), reinterpret_cast<const bf16*>(kn_w), H, Hkv, hd, layer, L_s,
                 max_blocks};

@@ -40,7 +40,7 @@ constexpr int UNIT_ROWS = 256;             // rows of W per work unit (2 UMMA ti
 constexpr int BK = 64;                     // 64 bf16 = 128 B = one swizzle atom row
 constexpr int SUB_BYTES = 128 * BK * 2;    // one 128x64 UMMA A tile (16 KB)
 constexpr int A_BYTES = 2 * SUB_BYTES;     // 32 KB per stage, contiguous in global
-constexpr int NUM_THREADS = 192;           // 6 warps
+constexpr int NUM_THREADS = 288;           // 9 warps: w0/w7 weights, w1 MMA, w2..w5 epilogue, w6/w8 activations
 constexpr int EPI_WARP0 = 2;
 
 enum Epilogue : int { EPI_STORE_BF16 = 0, EPI_RESID_ADD_F32 = 1, EPI_SILU_MUL = 2, EPI_LOGITS_ARGMAX = 3 };
@@ -263,59 +263,69 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 7) {
     if (lane == 0) {
-      // ---------------- producer: own 16 KB weight half-chunk + half of the X tile (multicast)
-      const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+      // ---------------- weight producers: own 16 KB half-chunk (pair) or 32 KB unit chunk,
+      // even / odd k-block steps from two threads.  Every copy is issued from its own
+      // thread pool: one thread's bulk / TMA copies are served at ~3.6 M ops/s
+      // (tools/sm_stream_probe.cu), which capped a CTA near 40-55 GB/s with one
+      // producer issuing both operands of every k-block.
+      const int par = warp == 0 ? 0 : 1;
+      const uint64_t pol_w = policy_evict_first();
       auto wsrc = [&](int wunit, int kb) {
         return a.w + (((size_t)wunit * a.kb + kb) * 2 + crank) * SUB_BYTES;   // NH halves from here
       };
-      // Weights do not depend on the previous kernel: stream the first stages
-      // of weights before waiting on it (the activation tiles wait).
-      int pre = 0;
-      {
-        Seg sg;
-        int it = 0;
-        for (int i = 0; it < C::STAGES && get_seg(a, lo, hi, i, sg, G, wk); ++i) {
-          const int wunit = sg.unit % a.n_units;
-          for (int kb = sg.kb0; kb < sg.kb1 && it < C::STAGES; ++kb, ++it) {
-            mbar_arrive_expect_tx(&full[it], C::STAGE);
-            bulk_load(sa + it * NH * SUB_BYTES, wsrc(wunit, kb), NH * SUB_BYTES, &full[it], pol_w);
-          }
-        }
-        pre = it;
-      }
-      pdl_wait();
-      PM_TRACE(1);   // producer past the dependency wait
+      // Weights do not depend on the previous kernel: they stream before (and
+      // regardless of) the dependency wait the activation producer does.
       int it = 0;
       Seg sg;
       for (int i = 0; get_seg(a, lo, hi, i, sg, G, wk); ++i) {
-        const int wunit = sg.unit % a.n_units, ttile = sg.unit / a.n_units;
+        const int wunit = sg.unit % a.n_units;
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
+          if ((it & 1) != par) continue;
           const int s = it % C::STAGES;
-          if (it >= pre) {
-            // both CTAs released the stage (the X multicast overwrites both)
-            if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
-            mbar_arrive_expect_tx(&full[s], C::STAGE);
-            bulk_load(sa + s * NH * SUB_BYTES, wsrc(wunit, kb), NH * SUB_BYTES, &full[s], pol_w);
-          }
-          if (PAIR)
-            tma_load_2d_mc(sb + s * C::B_BYTES + crank * (BN / 2) * 128, &tmap_x, &full[s], kb * BK,
-                           ttile * BN + crank * (BN / 2), (uint16_t)0x3, pol_x);
-          else
-            tma_load_2d(sb + s * C::B_BYTES, &tmap_x, &full[s], kb * BK, ttile * BN, pol_x);
+          // both CTAs released the stage (the X multicast overwrites both)
+          if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], C::STAGE);
+          bulk_load(sa + s * NH * SUB_BYTES, wsrc(wunit, kb), NH * SUB_BYTES, &full[s], pol_w);
         }
       }
+      PM_TRACE(1);
       // Every load of this CTA is issued: queue this CTA's share of the next
       // operation's first bytes behind them, so HBM keeps streaming through
       // this kernel's drain/exit and the next kernel's ramp (it reads from L2).
-      if (a.pf_bytes) {
+      if (a.pf_bytes && par == 0) {
+        pdl_wait();
         const unsigned long long share = ((a.pf_bytes / gridDim.x) + 15) & ~15ull;
         const unsigned long long b0 = share * blockIdx.x;
         const unsigned long long b1 = min(a.pf_bytes & ~15ull, b0 + share);
         for (unsigned long long o = b0; o < b1; o += 65536) {
           const uint32_t len = (uint32_t)min(65536ull, b1 - o);
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf + o), "r"(len) : "memory");
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 6 || warp == 8) {
+    // ---------------- activation producers (even / odd k-block steps): the X tile (pair: half
+    // of it, multicast to both CTAs)
+    pdl_wait();
+    if (lane == 0) {
+      const int par = warp == 6 ? 0 : 1;
+      const uint64_t pol_x = policy_evict_last();
+      int it = 0;
+      Seg sg;
+      for (int i = 0; get_seg(a, lo, hi, i, sg, G, wk); ++i) {
+        const int ttile = sg.unit / a.n_units;
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
+          if ((it & 1) != par) continue;
+          const int s = it % C::STAGES;
+          if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+          if (PAIR)
+            tma_load_2d_mc(sb + s * C::B_BYTES + crank * (BN / 2) * 128, &tmap_x, &full[s], kb * BK,
+                           ttile * BN + crank * (BN / 2), (uint16_t)0x3, pol_x);
+          else
+            tma_load_2d(sb + s * C::B_BYTES, &tmap_x, &full[s], kb * BK, ttile * BN, pol_x);
         }
       }
     }
