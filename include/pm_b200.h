@@ -34,6 +34,16 @@ int pm_tmap_encode_2d(void* tmap_out, const void* gaddr, unsigned long long inne
                       int swizzle128);
 int pm_host_alloc(unsigned long long bytes, void** out);
 int pm_host_free(void* p);
+/* NUMA node of device `device`'s PCIe attachment (sysfs; -1 unknown) */
+int pm_device_numa_node(int device, int* node);
+/* pinned + mapped host memory bound to NUMA node `numa_node` (mmap + mbind + cudaHostRegister; < 0: pm_host_alloc);
+ * free with pm_host_free_numa(p, bytes, numa_node) */
+int pm_host_alloc_numa(unsigned long long bytes, int numa_node, void** out);
+int pm_host_free_numa(void* p, unsigned long long bytes, int numa_node);
+/* eager decode offload: host_dev + offs[2i] <- pool + offs[2i+1], `bytes` each, one kernel (`ctas` CTAs) writing
+ * through the mapped replica; host_dev / offs are pm_host_device_ptr addresses; bytes % 16 == 0 */
+int pm_offload_rows(void* host_dev, const void* pool, const void* offs, int n, unsigned long long bytes, int ctas,
+                    void* stream);
 /* device address of pm_host_alloc memory (it is mapped: kernels may read it over PCIe) */
 int pm_host_device_ptr(void* host, void** dev);
 /* per-step metadata upload: dst[i][0..n[i]) <- src[i] (int32; src = pm_host_device_ptr addresses), a
@@ -105,6 +115,13 @@ int pm_gemm_split_event(void* event);
 int pm_prepare_attention(void);
 int pm_argmax_reduce(const float* val, const int* idx, int n_tiles, int M, int m_cap, int* out_ids,
                      int* tok_table, const int* slots, void* stream);
+
+/* ---- pipeline hop (pipeline.py) -------------------------------------------------------------------- */
+/* fp32 residual rows <-> bf16 wire format (n elements, n % 8 == 0) */
+int pm_hop_pack(const float* resid, void* out, long long n, void* stream);
+int pm_hop_unpack(const void* in, float* resid, long long n, void* stream);
+/* stage 0: tok_table[slots[i]] = ids[i]; slots may be mapped pinned host memory (pm_host_device_ptr) */
+int pm_scatter_tokens(const int* ids, const int* slots, int n, int* tok_table, void* stream);
 
 /* ---- cluster split-K projection (gemm_cl.cu): split-K reduction and epilogue in ONE kernel ----------
  * cluster = 2 * slices CTAs (pair = the two 128-row halves of a 256-row unit, sharing a multicast

@@ -21,6 +21,10 @@ _SIGS = {
     "pm_tmap_encode_2d": [_P, _P, _U64, _U64, _U64, C.c_uint, C.c_uint, _I],
     "pm_host_alloc": [_U64, C.POINTER(_P)],
     "pm_host_free": [_P],
+    "pm_device_numa_node": [_I, C.POINTER(_I)],
+    "pm_host_alloc_numa": [_U64, _I, C.POINTER(_P)],
+    "pm_host_free_numa": [_P, _U64, _I],
+    "pm_offload_rows": [_P, _P, _P, _I, _U64, _I, _P],
     "pm_host_device_ptr": [_P, C.POINTER(_P)],
     "pm_meta_upload": [_I, _P, _P, _P, _P],
     "pm_copy_pieces": [_P, _P, _P, _P, _I, _U64, _P],
@@ -43,6 +47,9 @@ _SIGS = {
     "pm_attn_blocks_per_split": [],
     "pm_prepare_gemm": [],
     "pm_prepare_attention": [],
+    "pm_hop_pack": [_P, _P, _LL, _P],
+    "pm_hop_unpack": [_P, _P, _LL, _P],
+    "pm_scatter_tokens": [_P, _P, _I, _P, _P],
     "pm_gemm_cl": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _I, _F, _P, _P, _P, _P, _P, _P,
                    _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _P],
     "pm_gemm_cl_max_clusters": [_I, _I, C.POINTER(_I)],

@@ -1,7 +1,11 @@
 // C-ABI utilities: version, error strings, TMA descriptor encoding, pinned
 // host memory, batched KV block copies for the offload engine.
 #include <cudaTypedefs.h>
+#include <stdio.h>
 #include <string.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include "common.cuh"
 
@@ -58,6 +62,54 @@ extern "C" int pm_copy_2d(void* dst, unsigned long long dpitch, const void* src,
 extern "C" int pm_host_alloc(unsigned long long bytes, void** out) {
   return (int)cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
 }
+// NUMA node of a CUDA device's PCIe attachment (sysfs), -1 when unknown.
+extern "C" int pm_device_numa_node(int device, int* node) {
+  *node = -1;
+  char bus[32];
+  cudaError_t e = cudaDeviceGetPCIBusId(bus, sizeof(bus), device);
+  if (e != cudaSuccess) return (int)e;
+  for (char* c = bus; *c; ++c)
+    if (*c >= 'A' && *c <= 'F') *c = (char)(*c - 'A' + 'a');
+  char path[128];
+  snprintf(path, sizeof(path), "/sys/bus/pci/devices/%s/numa_node", bus);
+  FILE* f = fopen(path, "r");
+  if (!f) return 0;
+  int n = -1;
+  if (fscanf(f, "%d", &n) != 1) n = -1;
+  fclose(f);
+  *node = n;
+  return 0;
+}
+
+// Pinned, mapped host memory placed on NUMA node `numa_node` (the node the
+// GPU's PCIe root hangs off, pm_device_numa_node): anonymous mmap, mbind
+// (MPOL_BIND) before first touch, then cudaHostRegister (portable | mapped).
+// numa_node < 0: plain pm_host_alloc.  Free with pm_host_free_numa.
+extern "C" int pm_host_alloc_numa(unsigned long long bytes, int numa_node, void** out) {
+  if (numa_node < 0) return (int)cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (p == MAP_FAILED) return (int)cudaErrorMemoryAllocation;
+  unsigned long mask[16] = {0};
+  if (numa_node < 16 * 64) {
+    mask[numa_node / 64] = 1ul << (numa_node % 64);
+    // MPOL_BIND = 2; a failure (no NUMA support in the kernel / container) leaves the default policy
+    syscall(SYS_mbind, p, bytes, 2, mask, (unsigned long)(16 * 64), 0u);
+  }
+  cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
+  if (e != cudaSuccess) {
+    munmap(p, bytes);
+    return (int)e;
+  }
+  *out = p;
+  return 0;
+}
+extern "C" int pm_host_free_numa(void* p, unsigned long long bytes, int numa_node) {
+  if (numa_node < 0) return (int)cudaFreeHost(p);
+  cudaError_t e = cudaHostUnregister(p);
+  munmap(p, bytes);
+  return (int)e;
+}
+
 // Device-side address of pinned host memory from pm_host_alloc (zero-copy reads).
 extern "C" int pm_host_device_ptr(void* host, void** dev) {
   return (int)cudaHostGetDevicePointer(dev, host, 0);
@@ -112,6 +164,42 @@ extern "C" int pm_meta_upload(int count, void* const* dst, const void* const* sr
   return (int)cudaLaunchKernelEx(&cfg, meta_upload_kernel, m);
 }
 extern "C" int pm_host_free(void* p) { return (int)cudaFreeHost(p); }
+
+namespace {
+// Eager decode offload (REF pipeline_sim.py:486-490): every row's new-token
+// KV (one contiguous `bytes` run in the block-first pool) is written straight
+// into its request's host-replica slot through the mapped pinned mapping --
+// one kernel instead of one DMA per row (the per-copy DMA setup capped the
+// copy engines near 10-14 GB/s on ~150 KB pieces).  offs[2i] = host offset,
+// offs[2i+1] = pool offset (mapped pinned memory, read over PCIe).
+__global__ void __launch_bounds__(256) offload_rows_kernel(uint8_t* __restrict__ host, const uint8_t* __restrict__ pool,
+                                                           const long long* __restrict__ offs, int n,
+                                                           unsigned long long bytes) {
+  const unsigned long long chunks = (bytes + 4095) / 4096;   // 4 KB per CTA iteration (256 x 16 B)
+  for (unsigned long long w = blockIdx.x; w < (unsigned long long)n * chunks; w += gridDim.x) {
+    const int row = (int)(w / chunks);
+    const unsigned long long c = (w % chunks) * 4096 + threadIdx.x * 16ull;
+    if (c >= bytes) continue;
+    const long long ho = __ldcv(offs + 2 * row), po = __ldcv(offs + 2 * row + 1);
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(pool + po + c));
+    *reinterpret_cast<uint4*>(host + ho + c) = v;
+  }
+}
+}  // namespace
+
+// host_dev: device address of the mapped replica (pm_host_device_ptr); offs:
+// device address of mapped pinned int64 pairs (host offset, pool offset);
+// bytes % 16 == 0.  `ctas` CTAs (a few suffice for PCIe rate; they co-reside
+// with the forward's kernels).
+extern "C" int pm_offload_rows(void* host_dev, const void* pool, const void* offs, int n, unsigned long long bytes,
+                               int ctas, void* stream) {
+  if (bytes % 16 || n < 0) return (int)cudaErrorInvalidValue;
+  if (n == 0) return 0;
+  offload_rows_kernel<<<ctas > 0 ? ctas : 32, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint8_t*>(host_dev), static_cast<const uint8_t*>(pool), static_cast<const long long*>(offs), n,
+      bytes);
+  return (int)cudaGetLastError();
+}
 
 // Batched copies of equal-sized KV pieces between two base addresses:
 // dst_base + dst_off[i] <- src_base + src_off[i], `bytes` each, in order, on

@@ -168,7 +168,64 @@ __global__ void argmax_reduce_kernel(const float* __restrict__ val, const int* _
   }
 }
 
+// Inter-stage activation hop (pipeline.py): the fp32 residual rows travel as
+// bf16 (half the NVLink bytes) -- pack before the send, unpack
+// into the receiving stage's residual.  8 elements per thread (16-byte bf16).
+__global__ void hop_pack_kernel(const float* __restrict__ x, bf16* __restrict__ y, long long n8) {
+  pdl_trigger();
+  pdl_wait();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+    const float4 a = reinterpret_cast<const float4*>(x)[2 * i], b = reinterpret_cast<const float4*>(x)[2 * i + 1];
+    reinterpret_cast<uint4*>(y)[i] = make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y),
+                                                pack_bf16(b.z, b.w));
+  }
+}
+__global__ void hop_unpack_kernel(const bf16* __restrict__ y, float* __restrict__ x, long long n8) {
+  pdl_trigger();
+  pdl_wait();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(y)[i];
+    reinterpret_cast<float4*>(x)[2 * i] = make_float4(bf16_lo(v.x), bf16_hi(v.x), bf16_lo(v.y), bf16_hi(v.y));
+    reinterpret_cast<float4*>(x)[2 * i + 1] = make_float4(bf16_lo(v.z), bf16_hi(v.z), bf16_lo(v.w), bf16_hi(v.w));
+  }
+}
+// Stage 0: greedy ids returned by the last stage -> the token table by slot.
+// `slots` may live in mapped pinned host memory (read over PCIe, no copy).
+__global__ void scatter_tokens_kernel(const int* __restrict__ ids, const int* __restrict__ slots, int n,
+                                      int* __restrict__ tok_table) {
+  pdl_trigger();
+  pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) tok_table[slots[i]] = ids[i];
+}
+
 }  // namespace
+
+extern "C" int pm_hop_pack(const float* resid, void* out, long long n, void* stream) {
+  if (n % 8) return (int)cudaErrorInvalidValue;
+  if (n == 0) return 0;
+  const long long n8 = n / 8;
+  const int blocks = (int)((n8 + 255) / 256 < 592 ? (n8 + 255) / 256 : 592);
+  cudaError_t e = launch_k(hop_pack_kernel, dim3(blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), resid,
+                           reinterpret_cast<bf16*>(out), n8);
+  return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
+}
+
+extern "C" int pm_hop_unpack(const void* in, float* resid, long long n, void* stream) {
+  if (n % 8) return (int)cudaErrorInvalidValue;
+  if (n == 0) return 0;
+  const long long n8 = n / 8;
+  const int blocks = (int)((n8 + 255) / 256 < 592 ? (n8 + 255) / 256 : 592);
+  cudaError_t e = launch_k(hop_unpack_kernel, dim3(blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
+                           reinterpret_cast<const bf16*>(in), resid, n8);
+  return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
+}
+
+extern "C" int pm_scatter_tokens(const int* ids, const int* slots, int n, int* tok_table, void* stream) {
+  if (n == 0) return 0;
+  cudaError_t e = launch_k(scatter_tokens_kernel, dim3((n + 255) / 256), dim3(256), 0,
+                           reinterpret_cast<cudaStream_t>(stream), ids, slots, n, tok_table);
+  return e != cudaSuccess ? (int)e : (int)cudaGetLastError();
+}
 
 extern "C" int pm_embed(const int* tok_table, const int* slots, const void* table, float* resid, int M,
                         int d, void* stream) {

@@ -76,6 +76,11 @@ class _MetaRing:
             pass
 
 
+def attn_rows_hint(n_requests: int, micro_batches: int) -> int:
+    """Rows of a typical rotation step: one micro-batch of the requests."""
+    return -(-n_requests // max(1, micro_batches))
+
+
 class DecodeEngine:
     def __init__(self, spec: ModelSpec, state: SchedulerState, cfg: ClusterConfig, params: EstimatorParams,
                  requests: dict, *, pp: int = 1, device="cuda", mode="dynamic", quota_tokens=0,
@@ -116,10 +121,11 @@ class DecodeEngine:
                                m_cap=self.m_cap, pool_blocks=pool_blocks, max_blocks=self.max_blocks,
                                n_slots=len(rids) + 1, device=self.dev, seed=seed, max_pos=self.max_pos,
                                keep_logical=record_logits,
-                               gemm_sms=ops.GEMM_CTAS_1LANE if lanes == 1 else None)
+                               gemm_sms=ops.GEMM_CTAS_1LANE if lanes == 1 else None,
+                               rows_hint=attn_rows_hint(self.m_cap, cfg.n))
             if record_logits:
                 ex.enable_logits()
-            rep = HostReplica(len(rids), self.max_blocks, ex.block_bytes)
+            rep = HostReplica(len(rids), self.max_blocks, ex.block_bytes, device=self.dev)
             self.stages.append((ex, KvEngine(ex, rep, self.slot_of, self.dev, timing=timing,
                                              low_priority_copies=copy_priority)))
         self.work_len = self.stages[0][0].aws.work_len
@@ -163,9 +169,11 @@ class DecodeEngine:
         g = torch.Generator(device=self.dev).manual_seed(seed + 1)
         first_tok = torch.randint(0, self.spec.vocab, (len(rids) + 1,), generator=g, device=self.dev,
                                   dtype=torch.int32)
+        # every stage's table starts equal: with several local stages the last
+        # stage's table is copied back to stage 0's after each step (the
+        # last -> first hop), so it must hold the not-yet-executed rows' tokens too
         for ex, kv in self.stages:
-            if ex.first:
-                ex.tok_table.copy_(first_tok)
+            ex.tok_table.copy_(first_tok)
         torch.cuda.synchronize()
         if how == "prefill":
             assert prompts is not None
@@ -177,10 +185,13 @@ class DecodeEngine:
         # keeps whatever the fresh pinned pages hold (zeros) -- values do not
         # change the timing
         for ex, kv in self.stages:
+            # seeded per stage (its first layer), so a rank hosting one stage of a
+            # pipeline holds the same KV as a process hosting all of them
+            gs = torch.Generator(device=self.dev).manual_seed(seed + 1 + 1000 * (ex.layers[0] + 1))
             pv = ex.pool.view(ex.pool_blocks, -1)
             for rid, blocks in self.control.alloc.tables.items():
                 idx = torch.tensor(blocks, device=self.dev)
-                pv[idx] = (torch.randn(len(blocks), pv.shape[1], generator=g, device=self.dev) * 0.5).to(torch.bfloat16)
+                pv[idx] = (torch.randn(len(blocks), pv.shape[1], generator=gs, device=self.dev) * 0.5).to(torch.bfloat16)
         torch.cuda.synchronize()
 
     def _prefill(self, prompts):
@@ -257,11 +268,20 @@ class DecodeEngine:
         prev_ev = None
         for si, (ex, kv) in enumerate(stages):
             st = kv.streams[lane]
-            if prev_ev is not None:
+            if si > 0:
+                # the inter-stage hop as the multi-GPU pipeline sends it: the
+                # previous stage packs its residual to bf16, this stage unpacks
+                prev = stages[si - 1][0]
+                hop = self._hop_buffer(lane, prev.resid)
+                n_el = M * prev.resid.shape[1]
+                _C.call("pm_hop_pack", _C.C.c_void_p(prev.resid.data_ptr()), _C.C.c_void_p(hop.data_ptr()), n_el,
+                        _C.C.c_void_p(stages[si - 1][1].streams[lane].cuda_stream))
+                prev_ev = torch.cuda.Event()
+                prev_ev.record(stages[si - 1][1].streams[lane])
                 st.wait_event(prev_ev)
+                _C.call("pm_hop_unpack", _C.C.c_void_p(hop.data_ptr()), _C.C.c_void_p(ex.resid.data_ptr()), n_el,
+                        _C.C.c_void_p(st.cuda_stream))
             with torch.cuda.stream(st):
-                if si > 0:
-                    ex.resid[:M].copy_(stages[si - 1][0].resid[:M])
                 ex.run(M, st, graphs=self.graphs, kv_tokens=kv_tokens)
                 if si == len(stages) - 1 and len(stages) > 1:
                     # greedy ids back to stage 0's token table (the last->first hop)
@@ -270,6 +290,15 @@ class DecodeEngine:
             prev_ev.record(st)
         if len(stages) > 1:
             stages[0][1].streams[lane].wait_event(prev_ev)
+
+    def _hop_buffer(self, lane, resid):
+        """bf16 wire buffer of the single-process stage hop (one per lane)."""
+        if not hasattr(self, "_hops"):
+            self._hops = {}
+        b = self._hops.get(lane)
+        if b is None:
+            b = self._hops[lane] = torch.empty(resid.numel(), dtype=torch.bfloat16, device=resid.device)
+        return b
 
     def start_phase(self, control: DecodeControl):
         """Begin a new decode phase with ``control`` (episode.py): the

@@ -17,27 +17,49 @@ Replaces the reference's simulated links (REF = reference
   prefetched requests' host copy; the step that first executes them waits on
   it (the stall the reference models at pipeline_sim.py:410-421).
 * Offload (step t): the new token's whole-stage KV (one contiguous slot per
-  row) HBM->host on the D2H stream right after the step's compute.
+  row) HBM->host on the D2H stream right after the step's compute -- one
+  kernel (pm_offload_rows) writing every row through the mapped replica
+  (PM_OFFLOAD_DMA=1: one cudaMemcpyAsync per row instead, for A/B).
+* The replica is pinned on the GPU's NUMA node (pm_host_alloc_numa).
 """
 
 from __future__ import annotations
+
+import os
 
 import numpy as np
 import torch
 
 from . import _C
 
+OFFLOAD_DMA = os.environ.get("PM_OFFLOAD_DMA", "0") == "1"
+OFFLOAD_CTAS = int(os.environ.get("PM_OFFLOAD_CTAS", "32"))
+
+
+def device_numa_node(device=None) -> int:
+    """NUMA node of the device's PCIe attachment (-1 unknown)."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    n = _C.C.c_int(-1)
+    _C.call("pm_device_numa_node", dev.index if dev.index is not None else torch.cuda.current_device(),
+            _C.C.byref(n))
+    return int(n.value)
+
 
 class HostReplica:
-    """Pinned host KV: ``slots`` request regions of ``max_blocks`` blocks."""
+    """Pinned host KV: ``slots`` request regions of ``max_blocks`` blocks, on
+    the NUMA node of ``device`` (``numa_node`` overrides; -1 = no binding)."""
 
-    def __init__(self, slots: int, max_blocks: int, block_bytes: int):
+    def __init__(self, slots: int, max_blocks: int, block_bytes: int, device=None, numa_node: int = None):
         self.slots, self.max_blocks, self.block_bytes = slots, max_blocks, block_bytes
         self.region_bytes = max_blocks * block_bytes
         self.nbytes = slots * self.region_bytes
+        self.numa_node = device_numa_node(device) if numa_node is None else numa_node
         ptr = _C.C.c_void_p()
-        _C.call("pm_host_alloc", self.nbytes, _C.C.byref(ptr))
+        _C.call("pm_host_alloc_numa", self.nbytes, self.numa_node, _C.C.byref(ptr))
         self.ptr = ptr.value
+        d = _C.C.c_void_p()
+        _C.call("pm_host_device_ptr", _C.C.c_void_p(self.ptr), _C.C.byref(d))
+        self.dev_ptr = d.value
 
     def offset(self, slot: int, block: int = 0) -> int:
         return slot * self.region_bytes + block * self.block_bytes
@@ -50,7 +72,7 @@ class HostReplica:
 
     def close(self):
         if self.ptr:
-            _C.call("pm_host_free", _C.C.c_void_p(self.ptr))
+            _C.call("pm_host_free_numa", _C.C.c_void_p(self.ptr), self.nbytes, self.numa_node)
             self.ptr = None
 
     def __del__(self):
@@ -95,6 +117,34 @@ class KvEngine:
         # lane (same-lane order is stream order); one array per lane so an
         # older toucher on lane B is not masked by a newer one on lane A.
         self.block_last_compute = [np.full(executor.pool_blocks, -1, dtype=np.int64)]
+        self._off_ring = None       # mapped pinned (host, pool) offset pairs of the offload kernel
+
+    def _offsets(self, n: int):
+        """A mapped pinned int64 [n][2] buffer for this step's offload offsets
+        (4-deep ring; a buffer is rewritten only after its kernel finished)."""
+        if self._off_ring is None:
+            import ctypes
+            cap = 2 * self.ex.m_cap
+            self._off_ring = []
+            for _ in range(4):
+                p = _C.C.c_void_p()
+                _C.call("pm_host_alloc", cap * 8, _C.C.byref(p))
+                d = _C.C.c_void_p()
+                _C.call("pm_host_device_ptr", p, _C.C.byref(d))
+                arr = np.frombuffer((ctypes.c_int64 * cap).from_address(p.value), dtype=np.int64)
+                self._off_ring.append([arr, d.value, None, p.value])
+            self._off_i = 0
+        slot = self._off_ring[self._off_i % 4]
+        self._off_i += 1
+        if slot[2] is not None:
+            slot[2].synchronize()
+        return slot
+    def __del__(self):
+        try:
+            for slot in self._off_ring or ():
+                _C.call("pm_host_free", _C.C.c_void_p(slot[3]))
+        except Exception:
+            pass
 
     def reset_phase(self):
         """New decode phase (episode.py): step numbers restart at 0, so the
@@ -246,11 +296,21 @@ class KvEngine:
             if self.timing:
                 rec["d2h_start"] = self._event()
                 rec["d2h_start"].record(s)
-            d = np.asarray(dst, dtype=np.int64)
-            sr = np.asarray(src, dtype=np.int64)
-            _C.call("pm_copy_pieces", _C.C.c_void_p(self.rep.ptr), _C.C.c_void_p(self.pool_ptr),
-                    d.ctypes.data_as(_C.C.c_void_p), sr.ctypes.data_as(_C.C.c_void_p), len(rows), tb,
-                    _C.C.c_void_p(s.cuda_stream))
+            if OFFLOAD_DMA:
+                d = np.asarray(dst, dtype=np.int64)
+                sr = np.asarray(src, dtype=np.int64)
+                _C.call("pm_copy_pieces", _C.C.c_void_p(self.rep.ptr), _C.C.c_void_p(self.pool_ptr),
+                        d.ctypes.data_as(_C.C.c_void_p), sr.ctypes.data_as(_C.C.c_void_p), len(rows), tb,
+                        _C.C.c_void_p(s.cuda_stream))
+            else:
+                slot = self._offsets(len(rows))
+                slot[0][0:2 * len(rows):2] = dst
+                slot[0][1:2 * len(rows):2] = src
+                _C.call("pm_offload_rows", _C.C.c_void_p(self.rep.dev_ptr), _C.C.c_void_p(self.pool_ptr),
+                        _C.C.c_void_p(slot[1]), len(rows), tb, OFFLOAD_CTAS, _C.C.c_void_p(s.cuda_stream))
+                ev = torch.cuda.Event()
+                ev.record(s)
+                slot[2] = ev
             done = self._event()
             done.record(s)
         rec["d2h_end"] = done

@@ -415,12 +415,14 @@ def attn_blocks_per_chunk() -> int:
 class AttnWorkspace:
     """Chunk partials [M][Hkv][chunks][8][hd] + (m, l), merge counters and the work list."""
 
-    def __init__(self, m_cap, Hkv, hd, max_blocks, device, cfg=None):
+    def __init__(self, m_cap, Hkv, hd, max_blocks, device, cfg=None, rows_hint=None):
+        """``rows_hint``: the rows a step usually carries (a micro-batch), which
+        sizes the launch-configuration choice; default ``m_cap``."""
         self.bpc = attn_blocks_per_chunk()
         self.Hkv = Hkv
         cuda = torch.cuda.is_available()
         if cfg is None:
-            cfg = choose_attn_cfg(m_cap, Hkv, hd, max_blocks, self.bpc) if cuda else -1
+            cfg = choose_attn_cfg(rows_hint or m_cap, Hkv, hd, max_blocks, self.bpc) if cuda else -1
         self.cfg = cfg
         self.workers = _C.lib().pm_attn_workers_cfg(hd, cfg) if cuda else 0
         self.max_chunks = max(1, -(-max_blocks // self.bpc))

@@ -34,12 +34,14 @@ class StageExecutor:
 
     def __init__(self, spec: ModelSpec, layers: range, *, first: bool, last: bool, m_cap: int,
                  pool_blocks: int, max_blocks: int, n_slots: int, device, seed: int = 0,
-                 max_pos: int = 4096, weights=None, keep_logical=False, gemm_sms: int = None):
+                 max_pos: int = 4096, weights=None, keep_logical=False, gemm_sms: int = None,
+                 rows_hint: int = None):
         self.spec, self.layers = spec, list(layers)
         self.first, self.last = first, last
         self.L_s = len(self.layers)
         self.m_cap, self.max_blocks, self.dev = m_cap, max_blocks, device
         self.gemm_sms = gemm_sms
+        self.rows_hint = rows_hint   # rows of a typical step (sizes the attention launch choice)
         s = spec
         self.logical = [] if keep_logical else None
         self.W = []
@@ -113,7 +115,7 @@ class StageExecutor:
             lin.sms = self.gemm_sms
         self.gws = ops.GemmWorkspace(m_cap, ops.GemmWorkspace.floats_needed(lins, m_cap),
                                      max(l.n_units for l in lins), self.lm_head.n_units if self.last else 1, device)
-        self.aws = ops.AttnWorkspace(m_cap, s.Hkv, s.hd, self.max_blocks, device)
+        self.aws = ops.AttnWorkspace(m_cap, s.Hkv, s.hd, self.max_blocks, device, rows_hint=self.rows_hint)
 
     def clone_lane(self) -> "StageExecutor":
         """A second executor over the same weights, KV pool and token table
@@ -247,6 +249,8 @@ class StageExecutor:
         if ops.CL_GEMM and M <= ops.CL_MAX_M:
             return (1 if self.first else 0) + 1 + 5 * self.L_s + (2 if self.last else 0)
         n = (1 if self.first else 0) + 1 + self.L_s * (2 + 1 + 2 + 2)
+        if self.split_norm:   # O / down: GEMM + reduce + a separate RMSNorm when the plan splits units
+            n += sum((w["o"].launches(M) > 1) + (w["down"].launches(M) > 1) for w in self.W)
         n += sum(w["gu"].launches(M) for w in self.W)
         if not self.last:
             n += self.W[-1]["down"].launches(M) - 2

@@ -11,20 +11,15 @@ WARPS = {1: 148 * 12, 2: 148 * 8}
 
 
 class _Lib:
-    def __init__(self, real):
-        self.real = real
+    """Only the worker-count query the cost model makes (no libpmb200.so needed)."""
 
     def pm_attn_workers_cfg(self, hd, cfg):
         return WARPS[cfg]
 
-    def __getattr__(self, name):
-        return getattr(self.real, name)
-
 
 @pytest.fixture
 def b200_workers(monkeypatch):
-    real = _C.lib()
-    monkeypatch.setattr(_C, "lib", lambda: _Lib(real))
+    monkeypatch.setattr(_C, "lib", lambda: _Lib())
     monkeypatch.delenv("PM_ATTN_CFG", raising=False)
 
 
@@ -35,6 +30,14 @@ def b200_workers(monkeypatch):
 ])
 def test_cost_model_picks_measured_winner(b200_workers, name, m_cap, max_blocks, want):
     assert ops.choose_attn_cfg(m_cap, 8, 128, max_blocks, 12) == want, name
+
+
+def test_engine_passes_rows_per_step():
+    """The engine sizes the choice by a micro-batch's rows (requests / micro-
+    batches), not by the workspace capacity (all requests)."""
+    from paper_2605_02189_b200.engine import attn_rows_hint
+    assert attn_rows_hint(512, 8) == 64 and attn_rows_hint(256, 2) == 128 and attn_rows_hint(256, 8) == 32
+    assert attn_rows_hint(10, 3) == 4
 
 
 def test_env_override(b200_workers, monkeypatch):
