@@ -239,8 +239,10 @@ def reference_engine_cost(n_iter=60):
 
 
 # ---------------------------------------------------------------- GPU leg
-def build_engine(config, rank=0, world=1, local=0):
-    """(engine, pipeline engine or None, spec, requests, params, description)."""
+def build_engine(config, rank=0, world=1, local=0, calibrate=True):
+    """(engine, pipeline engine or None, spec, requests, params, description).
+    ``calibrate``: the engine fits the planner's estimator on this GPU before
+    the run (DecodeEngine.recalibrate) and plans with the fit."""
     from paper_2605_02189_b200.engine import DecodeEngine
     if world > 1:
         # PP = N: one rank per stage (NCCL P2P), micro-batches >= stages
@@ -269,11 +271,11 @@ def build_engine(config, rank=0, world=1, local=0):
                             f"peak, 25% of requests start in host memory (offload on)")
         desc["parallelism"] = f"pp{pp}-stage{stage}"
         eng = DecodeEngine(spec, state, cfg, params, reqs, pp=pp, local_stages=[stage], device=f"cuda:{local}",
-                           kv_init="random", timing=True, seed=rank)
+                           kv_init="random", timing=True, seed=rank, calibrate=calibrate)
         return eng, None, spec, reqs, params, desc
     spec, state, cfg, params, reqs, desc = workload()
     eng = DecodeEngine(spec, state, cfg, params, reqs, device=f"cuda:{local}", kv_init="random",
-                       timing=True, seed=rank)
+                       timing=True, seed=rank, calibrate=calibrate)
     return eng, None, spec, reqs, params, desc
 
 
@@ -315,6 +317,8 @@ def measure_device(eng, steps, peaks, local=0, dist=None):
             d2h_busy += r["d2h_start"].elapsed_time(r["d2h_end"]) * 1e-3
     busy = h2d_busy + d2h_busy
     hidden = 1.0 - stall / busy if busy > 0 else 1.0
+    from paper_2605_02189_b200.calibrate import step_fidelity
+    within5, max_err, n_cmp = step_fidelity(kv.records[rec0:])
     M_avg = tokens / steps
     # decode roofline of the step: the slower of HBM bytes (weights
     # + the micro-batch's KV + new KV + activations) and evicted-KV bytes over
@@ -329,6 +333,7 @@ def measure_device(eng, steps, peaks, local=0, dist=None):
     return {
         "value": value, "tokens": tokens, "rows_per_step": M_avg, "dev_s": dev_s, "ms_per_step": dev_s / steps * 1e3,
         "hidden": hidden, "clocks": clocks.summary(),
+        "fidelity": {"steps_within_5pct": within5, "max_rel_err": max_err, "steps": n_cmp},
         "kv_transfer": {"h2d_bytes": h2d_b, "d2h_bytes": d2h_b, "h2d_busy_s": h2d_busy, "d2h_busy_s": d2h_busy,
                         "exposed_stall_s": stall, "h2d_GBps": bw_h2d / 1e9 if bw_h2d else None,
                         "d2h_GBps": bw_d2h / 1e9 if bw_d2h else None},
@@ -481,9 +486,9 @@ def free_engine(*objs):
     torch.cuda.empty_cache()
 
 
-def stage_summary(config, steps, warmup, peaks, local):
+def stage_summary(config, steps, warmup, peaks, local, calibrate=True):
     """One per-stage measurement (north-star key of the default line)."""
-    eng, _, spec, reqs, params, desc = build_engine(config, local=local)
+    eng, _, spec, reqs, params, desc = build_engine(config, local=local, calibrate=calibrate)
     for _ in range(warmup):
         assert eng.step() is not None
     r = measure_device(eng, steps, peaks, local)
@@ -491,7 +496,8 @@ def stage_summary(config, steps, warmup, peaks, local):
            "ms_per_step": r["ms_per_step"], "rows_per_step": r["rows_per_step"],
            "decode_roofline_frac": r["decode_roofline"]["frac"],
            "t_hbm_ms": r["decode_roofline"]["t_hbm_ms"], "t_pcie_ms": r["decode_roofline"]["t_pcie_ms"],
-           "kv_transfer_hidden_fraction": r["hidden"], "clocks": r["clocks"]}
+           "kv_transfer_hidden_fraction": r["hidden"], "clocks": r["clocks"],
+           "estimator_fidelity": r["fidelity"]}
     del eng
     free_engine()
     return out
@@ -510,7 +516,8 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks, peaks_src = load_peaks()
-    eng, peng, spec, reqs, params, desc = build_engine(args.config, rank, world, local)
+    eng, peng, spec, reqs, params, desc = build_engine(args.config, rank, world, local,
+                                                       calibrate=args.calibrate and world == 1)
     for _ in range(args.warmup):
         assert eng.step() is not None
     torch.cuda.synchronize()
@@ -546,14 +553,18 @@ def run_ours(args):
     if "gpu_launches" not in out:
         ex = eng.stages[0][0]
         out["gpu_launches"] = args.steps * (ex.kernels_per_step(eng.bucket(int(round(dev["rows_per_step"])))) + 1)
-    if rank == 0 and args.calibrate:
-        # on-box fit of the planner's estimator (REF model_core.py:158-182) from
-        # measured iterations of this engine, beside the analytic one the bench
-        # plans with (timing engine: it overwrites sampled KV slots)
-        from paper_2605_02189_b200.calibrate import calibrate_on_device, params_dict
-        cp, samples, err = calibrate_on_device(eng, reps=3)
-        out["estimator"] = {"planned_with": params_dict(params), "calibrated": params_dict(cp),
-                            "max_rel_fit_err": err, "samples": len(samples)}
+    if rank == 0:
+        # the planner's estimator: fitted on this GPU at engine start (REF
+        # model_core.py:158-182) and planned with; fidelity of its per-step
+        # prediction vs the measured step period over the timed steps
+        from paper_2605_02189_b200.calibrate import params_dict
+        est = {"planned_with": params_dict(eng.control.params), "analytic": params_dict(params),
+               "step_fidelity": dev["fidelity"],
+               "claim": "PAPER.md 667-669: >= 90% of steps within 5%, worst < 8%"}
+        if eng.calibration is not None:
+            est["max_rel_fit_err"] = eng.calibration["max_rel_fit_err"]
+            est["samples"] = len(eng.calibration["samples"])
+        out["estimator"] = est
     kv_ctx = int(np.mean([eng.control.state.lengths.get(r, 0) for r in range(len(reqs))]))
     M = int(round(dev["rows_per_step"]))
     if dist:
@@ -564,7 +575,7 @@ def run_ours(args):
     del eng, peng
     free_engine()
     if rank == 0 and world == 1 and args.config == "c2" and args.north_star:
-        ns = [stage_summary(c, args.steps, args.warmup, peaks, local) for c in ("c3-last", "c3-stage")]
+        ns = [stage_summary(c, args.steps, args.warmup, peaks, local, args.calibrate) for c in ("c3-last", "c3-stage")]
         worst = min(ns, key=lambda r: r["decode_roofline_frac"])
         out["north_star"] = {
             "target": "C3 (Qwen3-32B, PP=8, bs 512, seq 1024, offload on): >= 0.70 of the per-stage decode "
@@ -630,7 +641,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-kernel-timing", dest="kernel_timing", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-calibrate", dest="calibrate", action="store_false")
+    ap.add_argument("--no-calibrate", dest="calibrate", action="store_false",
+                    help="plan with the analytic estimator instead of the on-box fit")
     ap.add_argument("--no-north-star", dest="north_star", action="store_false")
     ap.add_argument("--config", default="c2", choices=["c2"] + sorted(STAGE_CONFIGS),
                     help="c2 (default): BASELINE configs[1] on one GPU; c3-*/c4-*: one PP=8 stage "

@@ -30,16 +30,22 @@ def default_grid(m_cap: int, max_len: int):
     return [(b, b * per) for b in bs for per in lens]
 
 
-def profile_samples(engine, grid=None, reps: int = 5, warmup: int = 2, seed: int = 0):
+def profile_samples(engine, grid=None, reps: int = 5, warmup: int = 2, seed: int = 0, pipelined: bool = None):
     """[(b, L, seconds)]: CUDA-event time of one decode iteration (every
     stage of ``engine``) with ``b`` rows whose prefix lengths sum to ``L``
-    (equal per row), on synthetic block tables over the engine's pool."""
+    (equal per row), on synthetic block tables over the engine's pool.
+
+    ``pipelined`` (default: the engine has several lanes): the STEP PERIOD of
+    back-to-back iterations alternating over the lanes, as the decode loop
+    runs them -- the time the planner's prefetch budget B * T_hat must cover
+    (REF scheduler.py:84-93); otherwise one isolated iteration."""
     eng = engine
+    lanes = eng.lanes if pipelined is None or pipelined else 1
     max_len = eng.max_blocks * 16 - 1
     grid = grid or default_grid(eng.m_cap, max_len)
     rng = np.random.default_rng(seed)
     n_blocks = eng.control.alloc.total
-    ex0, kv0 = eng.stages[0]
+    kv0 = eng.stages[0][1]
     out = []
     for b, L in grid:
         per = max(1, min(max_len, L // b))
@@ -47,27 +53,59 @@ def profile_samples(engine, grid=None, reps: int = 5, warmup: int = 2, seed: int
         tables = [list(rng.choice(n_blocks, nb, replace=nb > n_blocks)) for _ in range(b)]
         positions = [per] * b
         slots = [eng.trash_slot] * b
-        eng._fill_meta(tables, positions, slots)
+        for lane in range(lanes):
+            eng._fill_meta(tables, positions, slots, lane=lane)
+        torch.cuda.synchronize()
         times = []
         for i in range(warmup + reps):
             a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(kv0.compute)
-            eng._forward_all(b)
-            e.record(eng.stages[0][1].compute)
+            a.record(kv0.streams[0])
+            for st in kv0.streams[1:]:
+                st.wait_event(a)
+            n_it = 4 * lanes if lanes > 1 else 1
+            for k in range(n_it):
+                eng._forward_all(b, lane=k % lanes)
+            for st in kv0.streams[1:]:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                kv0.streams[0].wait_event(ev)
+            e.record(kv0.streams[0])
             torch.cuda.synchronize()
             if i >= warmup:
-                times.append(a.elapsed_time(e) * 1e-3)
+                times.append(a.elapsed_time(e) * 1e-3 / n_it)
         out.append((b, b * per, float(np.median(times))))
     return out
 
 
-def calibrate_on_device(engine, grid=None, reps: int = 5):
+def calibrate_on_device(engine, grid=None, reps: int = 5, pipelined: bool = None):
     """Fit (alpha, beta, delta) to measured iterations; returns
     (EstimatorParams, samples, max relative fit error)."""
-    samples = profile_samples(engine, grid, reps)
+    samples = profile_samples(engine, grid, reps, pipelined=pipelined)
     params = calibrate_estimator(samples)
     err = max(abs(params.alpha * b + params.beta * L + params.delta - t) / t for b, L, t in samples)
     return params, samples, err
+
+
+def step_fidelity(records, t0: int = 0):
+    """Per-step estimator fidelity of a decode run (the paper's claim, PAPER.md
+    667-669): the planner's predicted step time vs the measured step period
+    (end of step t minus end of step t-1, CUDA events on the compute streams)
+    for every step after ``t0``.  Returns (fraction within 5 %, max relative
+    error, steps compared)."""
+    recs = sorted((r for r in records if "end" in r and r.get("info", {}).get("plan") is not None),
+                  key=lambda r: r["t"])
+    errs = []
+    for prev, cur in zip(recs, recs[1:]):
+        if cur["t"] != prev["t"] + 1 or cur["t"] < t0:
+            continue
+        meas = prev["end"].elapsed_time(cur["end"]) * 1e-3
+        pred = cur["info"]["plan"].predicted_exec_seconds
+        if meas > 0:
+            errs.append(abs(pred - meas) / meas)
+    if not errs:
+        return None, None, 0
+    errs = np.asarray(errs)
+    return float((errs <= 0.05).mean()), float(errs.max()), len(errs)
 
 
 def write_samples_csv(path: str, samples) -> None:

@@ -87,7 +87,7 @@ class DecodeEngine:
                  seed: int = 0, m_cap: int = None, timing=True, kv_init="random", prompts=None,
                  record_logits=False, max_pos=None, trace: EventTrace = None, graphs: bool = True,
                  local_stages=None, staging_pool_requests: int = 2, lanes: int = None,
-                 copy_priority: bool = True):
+                 copy_priority: bool = True, calibrate: bool = False):
         """``local_stages``: which of the ``pp`` stages this process hosts
         (default all; one rank per stage under torchrun, see pipeline.py)."""
         self.spec, self.cfg, self.params = spec, cfg, params
@@ -158,6 +158,12 @@ class DecodeEngine:
                 for ex, kv in stages:
                     for Mb in range(16, self.m_cap + 16, 16):
                         ex.capture(min(Mb, self.m_cap), kv.streams[li])
+        self.calibration = None
+        if calibrate:
+            # on-box estimator fit (REF model_core.py:158-182) BEFORE the KV is
+            # seeded (the profile appends KV at synthetic positions), then the
+            # planner plans with it: T_hat -> the prefetch budget B * T_hat
+            self.recalibrate()
         self._init_kv(kv_init, prompts, seed)
 
     # ------------------------------------------------------------------ setup
@@ -290,6 +296,19 @@ class DecodeEngine:
             prev_ev.record(st)
         if len(stages) > 1:
             stages[0][1].streams[lane].wait_event(prev_ev)
+
+    def recalibrate(self, grid=None, reps: int = 3):
+        """Fit (alpha, beta, delta) to this engine's measured step periods (its
+        lane mode included) and plan every later step with the fit."""
+        from .calibrate import calibrate_on_device, default_grid
+        if grid is None:   # batch sizes around a micro-batch's rows, lengths up to the longest request
+            grid = default_grid(min(self.m_cap, 2 * attn_rows_hint(self.m_cap, self.cfg.n)), self.max_blocks * 16 - 1)
+        params, samples, err = calibrate_on_device(self, grid, reps)
+        self.params = params
+        self.control.params = params
+        self.calibration = {"params": params, "samples": samples, "max_rel_fit_err": err}
+        torch.cuda.synchronize()
+        return params
 
     def _hop_buffer(self, lane, resid):
         """bf16 wire buffer of the single-process stage hop (one per lane)."""
