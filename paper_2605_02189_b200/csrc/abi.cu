@@ -7,6 +7,8 @@
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 extern "C" int pm_abi_version(void) { return 1; }
@@ -209,17 +211,36 @@ extern "C" int pm_offload_rows(void* host_dev, const void* pool, const void* off
 extern "C" int pm_copy_pieces(void* dst_base, const void* src_base, const long long* dst_off,
                               const long long* src_off, int n, unsigned long long bytes, void* stream) {
   auto st = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<void*> dsts, srcs;
+  std::vector<size_t> sizes;
   int i = 0;
   while (i < n) {
     int j = i + 1;
     while (j < n && dst_off[j] == dst_off[j - 1] + (long long)bytes &&
            src_off[j] == src_off[j - 1] + (long long)bytes)
       ++j;
-    cudaError_t e = cudaMemcpyAsync(static_cast<char*>(dst_base) + dst_off[i],
-                                    static_cast<const char*>(src_base) + src_off[i],
-                                    bytes * (size_t)(j - i), cudaMemcpyDefault, st);
-    if (e != cudaSuccess) return (int)e;
+    dsts.push_back(static_cast<char*>(dst_base) + dst_off[i]);
+    srcs.push_back(const_cast<char*>(static_cast<const char*>(src_base)) + src_off[i]);
+    sizes.push_back(bytes * (size_t)(j - i));
     i = j;
+  }
+  if (dsts.empty()) return 0;
+  // One batched submission (CUDA 12.8+): the driver sets the whole step's
+  // copies up at once instead of one cudaMemcpyAsync call per run.
+  static const int batch = getenv("PM_COPY_BATCH") ? atoi(getenv("PM_COPY_BATCH")) : 1;   // A/B
+  if (batch && dsts.size() > 1) {
+    cudaMemcpyAttributes attr = {};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t attr_idx = 0, fail = 0;
+    cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &attr_idx, 1,
+                                         &fail, st);
+    if (e == cudaSuccess) return 0;
+    cudaGetLastError();   // not supported here: fall back to one call per run
+  }
+  for (size_t k = 0; k < dsts.size(); ++k) {
+    cudaError_t e = cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyDefault, st);
+    if (e != cudaSuccess) return (int)e;
   }
   return 0;
 }

@@ -17,9 +17,12 @@ Replaces the reference's simulated links (REF = reference
   prefetched requests' host copy; the step that first executes them waits on
   it (the stall the reference models at pipeline_sim.py:410-421).
 * Offload (step t): the new token's whole-stage KV (one contiguous slot per
-  row) HBM->host on the D2H stream right after the step's compute -- one
-  kernel (pm_offload_rows) writing every row through the mapped replica
-  (PM_OFFLOAD_DMA=1: one cudaMemcpyAsync per row instead, for A/B).
+  row) HBM->host on the D2H copy-engine stream right after the step's
+  compute, all rows submitted as one cudaMemcpyBatchAsync (pm_copy_pieces).
+  PM_OFFLOAD_DMA=0 selects the SM-side variant (pm_offload_rows: a kernel
+  storing through the mapped replica) for A/B only -- measured at ~1 GB/s
+  on B200 (SM stores to mapped host memory), which made C2 4x slower
+  (profiles/r2/offload_ab.md).
 * The replica is pinned on the GPU's NUMA node (pm_host_alloc_numa).
 """
 
@@ -32,7 +35,7 @@ import torch
 
 from . import _C
 
-OFFLOAD_DMA = os.environ.get("PM_OFFLOAD_DMA", "0") == "1"
+OFFLOAD_DMA = os.environ.get("PM_OFFLOAD_DMA", "1") == "1"
 OFFLOAD_CTAS = int(os.environ.get("PM_OFFLOAD_CTAS", "32"))
 
 
@@ -53,7 +56,10 @@ class HostReplica:
         self.slots, self.max_blocks, self.block_bytes = slots, max_blocks, block_bytes
         self.region_bytes = max_blocks * block_bytes
         self.nbytes = slots * self.region_bytes
-        self.numa_node = device_numa_node(device) if numa_node is None else numa_node
+        if numa_node is None:   # PM_HOST_NUMA overrides (-1 = no binding; A/B)
+            env = os.environ.get("PM_HOST_NUMA")
+            numa_node = int(env) if env is not None else device_numa_node(device)
+        self.numa_node = numa_node
         ptr = _C.C.c_void_p()
         _C.call("pm_host_alloc_numa", self.nbytes, self.numa_node, _C.C.byref(ptr))
         self.ptr = ptr.value
