@@ -224,20 +224,6 @@ extern "C" int pm_copy_pieces(void* dst_base, const void* src_base, const long l
     sizes.push_back(bytes * (size_t)(j - i));
     i = j;
   }
-  if (dsts.empty()) return 0;
-  // One batched submission (CUDA 12.8+): the driver sets the whole step's
-  // copies up at once instead of one cudaMemcpyAsync call per run.
-  static const int batch = getenv("PM_COPY_BATCH") ? atoi(getenv("PM_COPY_BATCH")) : 1;   // A/B
-  if (batch && dsts.size() > 1) {
-    cudaMemcpyAttributes attr = {};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t attr_idx = 0, fail = 0;
-    cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &attr_idx, 1,
-                                         &fail, st);
-    if (e == cudaSuccess) return 0;
-    cudaGetLastError();   // not supported here: fall back to one call per run
-  }
   for (size_t k = 0; k < dsts.size(); ++k) {
     cudaError_t e = cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyDefault, st);
     if (e != cudaSuccess) return (int)e;

@@ -18,7 +18,8 @@ Replaces the reference's simulated links (REF = reference
   it (the stall the reference models at pipeline_sim.py:410-421).
 * Offload (step t): the new token's whole-stage KV (one contiguous slot per
   row) HBM->host on the D2H copy-engine stream right after the step's
-  compute, all rows submitted as one cudaMemcpyBatchAsync (pm_copy_pieces).
+  compute, one cudaMemcpyAsync per run of contiguous rows (pm_copy_pieces,
+  submitted from C).
   PM_OFFLOAD_DMA=0 selects the SM-side variant (pm_offload_rows: a kernel
   storing through the mapped replica) for A/B only -- measured at ~1 GB/s
   on B200 (SM stores to mapped host memory), which made C2 4x slower
