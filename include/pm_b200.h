@@ -69,27 +69,42 @@ int pm_rmsnorm(const float* x, const void* w, void* y, int M, int d, float eps, 
  * halves) per 256-row unit. */
 int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok, int bn,
             int grid, int cta_pair, int epilogue, void* out, int ld_out, float* ws, int max_segs, float* amax_val,
-            int* amax_idx, int m_cap, const void* prefetch, unsigned long long prefetch_bytes, void* stream);
+            int* amax_idx, int m_cap, const void* prefetch, unsigned long long prefetch_bytes,
+            unsigned long long prefetch_span, int* fix_counters, const int* fix_units, int n_fix, void* stream);
 /* prefetch/prefetch_bytes: optional region the NEXT operation reads first; it is pulled into L2 while
- * this GEMM drains (keeps HBM busy across the kernel boundary); NULL/0 for none. */
+ * this GEMM drains (keeps HBM busy across the kernel boundary); NULL/0 for none.  prefetch_span = 0:
+ * the contiguous [prefetch, +prefetch_bytes); > 0: one stripe of prefetch_bytes / grid per CTA, stripe c
+ * at prefetch + c * prefetch_span / grid -- the first bytes of every stream-K worker's range when the
+ * next operation is a GEMM over prefetch_span bytes of packed weight (its workers start at evenly spaced
+ * k-blocks). */
+/* fix_counters = NULL: split units are finished by a post kernel (launched on `stream` after the GEMM).
+ * fix_counters = int[2 * n_units] (zero at rest, left zero): the GEMM kernel finishes them itself --
+ * fixup tasks over the n_fix units in fix_units (the split units, pm_gemm_fix_units; every unit for
+ * pm_gemm_qkv_rope), equal shares per CTA, each waiting on its unit's segment arrivals.  Needs every
+ * CTA of the grid resident at once (one stream of dependent kernels, not two concurrent lanes) and
+ * m_tok <= bn. */
 /* residual projection (O / down) fused with the next RMSNorm: resid += X W^T (fp32), then
  * xn = RMSNorm(resid) * norm_w (bf16) per row; row_counters int[m_cap], zero at rest, left zero.
  * split_norm = 0: the last unit to finish a row normalises it inside the fixup kernel;
  * 1: fixup kernel, then a row-parallel RMSNorm kernel (same result, bit for bit) */
 int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
                           int bn, int grid, int cta_pair, float* resid, float* ws, int max_segs, int m_cap, const void* prefetch,
-                          unsigned long long prefetch_bytes, const void* norm_w, void* xn, float eps,
-                          int* row_counters, int split_norm, void* stream);
+                          unsigned long long prefetch_bytes, unsigned long long prefetch_span, const void* norm_w, void* xn, float eps,
+                          int* row_counters, int split_norm, int* fix_counters, const int* fix_units, int n_fix,
+                          void* stream);
 /* QKV projection fused with (Qwen3 q/k RMSNorm) + RoPE + paged KV append (pm_qkv_rope_append's contract);
  * qkv_out [m_cap][n_out] bf16 is scratch */
 int pm_gemm_qkv_rope(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok, int bn,
                      int grid, int cta_pair, void* qkv_out, float* ws, int max_segs, int m_cap, const void* prefetch,
-                     unsigned long long prefetch_bytes, void* q_out, void* pool, const int* block_table,
+                     unsigned long long prefetch_bytes, unsigned long long prefetch_span, int* fix_counters,
+                     const int* fix_units, int n_fix, void* q_out, void* pool, const int* block_table,
                      const int* positions, const float* rope, const void* qn_w, const void* kn_w, int H, int Hkv,
                      int hd, int layer, int L_s, int max_blocks, float eps, void* stream);
 /* stream-K geometry helpers over `workers` (= grid, or grid / 2 in pair mode) */
 int pm_gemm_split_units(long long total, int kb, int workers);
 int pm_gemm_max_segments(long long total, int kb, int workers);
+/* the units a stream-K partition splits (ascending) into out[], returns their count */
+int pm_gemm_fix_units(long long total, int kb, int workers, int* out);
 int pm_qkv_rope_append(const void* qkv, void* q_out, void* pool, const int* block_table, const int* positions,
                        const float* rope, const void* qn_w, const void* kn_w, int M, int H, int Hkv, int hd,
                        int layer, int L_s, int max_blocks, float eps, void* stream);

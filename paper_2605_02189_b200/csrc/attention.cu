@@ -33,7 +33,7 @@
 namespace {
 
 constexpr int MAX_G = 8;
-constexpr int MAX_BPC = 16;   // KV blocks per work item (pm_attn_blocks_per_split)
+constexpr int MAX_BPC = 32;   // KV blocks per work item (pm_attn_blocks_per_split)
 
 PM_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -128,8 +128,15 @@ PM_DEV void load_q(const AttnArgs& a, const Cursor& c, int lane, uint32_t (&q)[H
   }
 }
 
+// PM_ATTN_MAXNREG (build-time A/B): cap the registers so a small fixup CTA
+// of the other lane can share the SM with an attention CTA
+#ifdef PM_ATTN_MAXNREG
+#define PM_ATTN_BOUNDS(T) __maxnreg__(PM_ATTN_MAXNREG)
+#else
+#define PM_ATTN_BOUNDS(T) __launch_bounds__(T)
+#endif
 template <int HD, int WARPS, int STAGES>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void PM_ATTN_BOUNDS(WARPS * 32)
 paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
   using C = AttnCfg<HD, WARPS, STAGES>;
   constexpr int HALVES = HD / 64;
@@ -512,8 +519,8 @@ extern "C" int pm_attn_blocks_per_split(void) {
   static int bpc = 0;
   if (!bpc) {
     const char* e = getenv("PM_ATTN_BPC");  // tuning override
-    bpc = e ? atoi(e) : 12;
-    if (bpc < 1 || bpc > MAX_BPC) bpc = 12;
+    bpc = e ? atoi(e) : 24;   // measured best on the C2 / C3 / C4 benches (profiles/r2/attention_chunks.md)
+    if (bpc < 1 || bpc > MAX_BPC) bpc = 24;
   }
   return bpc;
 }

@@ -62,10 +62,41 @@ struct GemmArgs {
   int m_cap;
   const uint8_t* pf;  // bytes the NEXT operation streams first: prefetched into L2 during this tail
   unsigned long long pf_bytes;
+  unsigned long long pf_span;   // > 0: stripe c of pf_bytes / grid at pf + c * pf_span / grid
+  unsigned int pf_ahead;        // bytes per CTA of its own range past the ring pulled into L2 once the ring is full
   long long total;    // units * tok_tiles * kb
   int debug;          // profiling only: bit0 skip epilogue math, bit2 skip partial stores, bit3 trace,
                       // bit4 skip the fixup/post kernel (bits 5/6/7: only reduce / resid-norm / qkv-rope)
+  int fused;          // 1: split units are finished inside this kernel (fused_fixup), no post kernel
+  int post;           // Post: what the fixup applies (plain epilogue / residual + RMSNorm / q-k norm + RoPE)
+  int* unit_cnt;      // fused: [units] segment arrivals, then [units] finished fixup tasks (zero at rest)
+  const int* fix_units;   // fused: the units with fixup tasks (split units; every unit for the QKV post)
+  int n_fix;
 };
+
+enum Post : int { POST_NONE = 0, POST_RESID_NORM = 1, POST_QKV_ROPE = 2 };
+
+struct NormArgs {
+  const bf16* w;      // [d] RMSNorm weight
+  bf16* xn;           // [m_cap][d] normalised output (the next GEMM's TMA source)
+  int* row_cnt;       // [m_cap] arrival counts, zero at rest
+  int n_split;        // units of this launch with > 1 segment (all arrive once per row)
+  float eps;
+};
+
+struct RopeArgs {
+  bf16* q_out;              // [M][H][hd]
+  bf16* pool;               // block-first KV pool
+  const int* block_table;   // [M][max_blocks]
+  const int* positions;     // [M]
+  const float* rope;        // [pos][hd] cos | sin
+  const bf16* qn_w;         // [hd] or null
+  const bf16* kn_w;
+  int H, Hkv, hd, layer, L_s, max_blocks;
+  float eps;
+};
+
+
 
 // NH = 128-row halves of the 256-row unit one CTA computes: 2 (a CTA owns the
 // unit) or 1 (a 2-CTA cluster owns it; the X tile is split and multicast).
@@ -218,9 +249,330 @@ PM_DEV unsigned long long gtimer() {
     if ((a.debug & 8) && blockIdx.x < 148) g_gemm_trace[blockIdx.x * 8 + (slot)] = gtimer(); \
   } while (0)
 
-template <int BN, int NH>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
+// ---------------------------------------------------------------- in-kernel split-K fixup (fused mode)
+// Single-lane engines finish the units the stream-K partition splits inside
+// the GEMM kernel instead of a post kernel.  Every split segment's CTA stores
+// its fp32 partial and arrives on the unit's count (release); once its own
+// segments are done, every CTA takes an equal, contiguous share of the fixup
+// tasks (a task = one listed unit x FIX_COLS token columns), waits until the
+// unit's segments have all arrived (acquire), sums the partials in segment
+// order -- the post kernels' order, so results are bit-identical -- and
+// applies the epilogue: bf16 store, SiLU*up, logits + argmax tiles, residual
+// add (+ the next RMSNorm of every row whose 128-row tiles have all landed,
+// by the CTA that lands the last one), or q/k RMSNorm + RoPE + paged KV append
+// (QKV lists every unit; whole ones are read back from the stored bf16).
+// The waits assume every CTA of the grid is resident: grid <= #SMs at one CTA
+// per SM and nothing else on the SMs waits on this grid -- one stream of
+// dependent kernels.  Two lanes interleave two persistent grids on the SMs, so
+// only single-lane engines launch it (ops.Linear.fused).
+constexpr int FIX_COLS = 8;   // token columns per task; 128 threads = 2 columns x 64 threads (4 rows each)
+
+PM_DEV int useg(const GemmArgs& a, int unit, long long G) {
+  const long long T = a.total;
+  return (int)(owner_of((long long)(unit + 1) * a.kb - 1, T, G) - owner_of((long long)unit * a.kb, T, G) + 1);
+}
+PM_DEV void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+PM_DEV int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+PM_DEV int atom_add_acq_rel(int* p, int v) {
+  int prev;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(prev) : "l"(p), "r"(v) : "memory");
+  return prev;
+}
+
+// RMSNorm of one fp32 row by the 128 epilogue threads with rmsnorm_kernel's
+// arithmetic and reduction tree (thread tid plays its virtual threads tid and
+// tid + 128): bit-identical to the unfused norm.  V4 = ceil(d / 1024).
+template <int V4>
+PM_DEV void norm_row128(const float* x, const bf16* w, bf16* y, int d, float eps, float* red, int tid) {
+  const int n4 = d / 4, lane = tid & 31;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float4 va[V4], vb[V4];
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const int ia = tid + i * 256, ib = tid + 128 + i * 256;
+    va[i] = ia < n4 ? __ldcg(x4 + ia) : make_float4(0.f, 0.f, 0.f, 0.f);
+    vb[i] = ib < n4 ? __ldcg(x4 + ib) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float sa = 0.f, sb = 0.f;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    sa += va[i].x * va[i].x + va[i].y * va[i].y + va[i].z * va[i].z + va[i].w * va[i].w;
+    sb += vb[i].x * vb[i].x + vb[i].y * vb[i].y + vb[i].z * vb[i].z + vb[i].w * vb[i].w;
+  }
+  sa = warp_sum(sa);
+  sb = warp_sum(sb);
+  if (lane == 0) { red[tid >> 5] = sa; red[(tid >> 5) + 4] = sb; }
+  epi_bar();
+  float t = lane < 8 ? red[lane] : 0.f;
+  t = warp_sum(t);
+  epi_bar();   // red is reused by the next row
+  const float r = rsqrtf(t / (float)d + eps);
+  const uint2* wr = reinterpret_cast<const uint2*>(w);
+  uint2* yr = reinterpret_cast<uint2*>(y);
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const int ia = tid + i * 256, ib = tid + 128 + i * 256;
+    if (ia < n4) {
+      const uint2 ww = wr[ia];
+      yr[ia] = make_uint2(pack_bf16(va[i].x * r * bf16_lo(ww.x), va[i].y * r * bf16_hi(ww.x)),
+                          pack_bf16(va[i].z * r * bf16_lo(ww.y), va[i].w * r * bf16_hi(ww.y)));
+    }
+    if (ib < n4) {
+      const uint2 ww = wr[ib];
+      yr[ib] = make_uint2(pack_bf16(vb[i].x * r * bf16_lo(ww.x), vb[i].y * r * bf16_hi(ww.x)),
+                          pack_bf16(vb[i].z * r * bf16_lo(ww.y), vb[i].w * r * bf16_hi(ww.y)));
+    }
+  }
+}
+PM_DEV void norm_rows128(const GemmArgs& a, const NormArgs& na, const int* rows, int nrows, float* red, int tid) {
+  const float* x = reinterpret_cast<const float*>(a.out);
+  const int d = a.n_out;
+  for (int j = 0; j < nrows; ++j) {
+    const int m = rows[j];
+    if (d <= 4096) norm_row128<4>(x + (size_t)m * a.ld_out, na.w, na.xn + (size_t)m * d, d, na.eps, red, tid);
+    else if (d <= 5120) norm_row128<5>(x + (size_t)m * a.ld_out, na.w, na.xn + (size_t)m * d, d, na.eps, red, tid);
+    else norm_row128<8>(x + (size_t)m * a.ld_out, na.w, na.xn + (size_t)m * d, d, na.eps, red, tid);
+  }
+}
+
+// Residual tiles landed for token columns [c_lo, c_hi) of the tile (`add`
+// 128-row tiles each): arrive on each row's count; the arrivals that complete
+// a row (2 x n_units tiles) normalise it.  Called by all 128 epilogue threads
+// after the tile's residual stores.
+PM_DEV void resid_arrive(const GemmArgs& a, const NormArgs& na, int tok_base, int c_lo, int c_hi, int add,
+                         int* list, float* red, int tid) {
+  const int target = 2 * a.n_units;
+  epi_bar();   // every thread's residual stores precede the releases below
+  if (tid == 0) list[0] = 0;
+  epi_bar();
+  for (int c = c_lo + tid; c < c_hi; c += 128) {
+    const int row = tok_base + c;
+    if (atom_add_acq_rel(na.row_cnt + row, add) + add == target) {
+      na.row_cnt[row] = 0;
+      list[1 + atomicAdd(&list[0], 1)] = row;
+    }
+  }
+  epi_bar();
+  const int n = list[0];
+  if (n) norm_rows128(a, na, list + 1, n, red, tid);
+  epi_bar();   // list reused by the next call
+}
+
+// One column c of the QKV task (64 threads x 4 features; the v4 post kernel's
+// lane layout), x = the column's 4 features as the unfused qkv buffer holds them.
+template <int HD>
+PM_DEV void qkv_rope_col(const GemmArgs& a, const RopeArgs& ra, int wunit, int m, int t, int lane, float (&x)[4]) {
+  constexpr int HL = HD / 4;
+  const int r = 4 * t, n = wunit * UNIT_ROWS + r;
+  const bool row_ok = n < a.n_out;
+  const int hg = n / HD, d = n % HD;
+  const bool is_q = hg < ra.H, is_k = !is_q && hg < ra.H + ra.Hkv;
+  const bf16* nw = is_q ? ra.qn_w : (is_k ? ra.kn_w : nullptr);
+  const int pos = ra.positions[m];
+  const int fi = (lane & (HL / 2 - 1)) * 4;
+  float4 cs = make_float4(0.f, 0.f, 0.f, 0.f), sn = cs;
+  if (is_q || is_k) {
+    cs = *reinterpret_cast<const float4*>(ra.rope + (size_t)pos * HD + fi);
+    sn = *reinterpret_cast<const float4*>(ra.rope + (size_t)pos * HD + HD / 2 + fi);
+  }
+  float w4[4] = {1.f, 1.f, 1.f, 1.f};
+  if (nw) {
+    const uint2 ww = *reinterpret_cast<const uint2*>(nw + d);
+    w4[0] = bf16_lo(ww.x); w4[1] = bf16_hi(ww.x); w4[2] = bf16_lo(ww.y); w4[3] = bf16_hi(ww.y);
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) ss += x[e] * x[e];
+#pragma unroll
+  for (int o = HL / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (nw) {
+    const float rr = rsqrtf(ss / (float)HD + ra.eps);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = x[e] * rr * w4[e];
+  }
+  const bool lo_half = (lane & (HL - 1)) < HL / 2;
+  const float c4[4] = {cs.x, cs.y, cs.z, cs.w}, s4[4] = {sn.x, sn.y, sn.z, sn.w};
+  float y[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float partner = __shfl_xor_sync(0xffffffffu, x[e], HL / 2);
+    y[e] = lo_half ? (x[e] * c4[e] - partner * s4[e]) : (x[e] * c4[e] + partner * s4[e]);
+  }
+  if (is_q || is_k) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = y[e];
+  }
+  if (!row_ok) return;
+  bf16* dst;
+  if (is_q) {
+    dst = ra.q_out + ((size_t)m * ra.H + hg) * HD + d;
+  } else {
+    const int kv = is_k ? 0 : 1;
+    const int g = is_k ? hg - ra.H : hg - ra.H - ra.Hkv;
+    const int slot_off = ra.block_table[(size_t)m * ra.max_blocks + pos / 16];
+    const size_t tok_stride = (size_t)ra.L_s * 2 * ra.Hkv * HD;
+    dst = ra.pool + ((size_t)slot_off * 16 + (pos & 15)) * tok_stride + (((size_t)ra.layer * 2 + kv) * ra.Hkv + g) * HD + d;
+  }
+  *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]));
+}
+
+// The fixup phase of one CTA (128 epilogue threads).  list/n_list: the
+// launch's task units (a.fix_units), G = stream-K workers, NHW = CTAs per
+// worker (2 in pair mode: both halves arrive).
+template <int BN>
+PM_DEV void fused_fixup(const GemmArgs& a, const NormArgs& na, const RopeArgs& ra, long long G, int NHW, int* slist,
+                        float* red, int tid) {
+  const int lane = tid & 31;
+  const int groups = (a.m_tok + FIX_COLS - 1) / FIX_COLS;   // tok_tiles == 1 in fused mode
+  const long long T = (long long)a.n_fix * groups;
+  const long long t0 = (long long)blockIdx.x * T / gridDim.x, t1 = (long long)(blockIdx.x + 1) * T / gridDim.x;
+  const int units = a.n_units;
+  for (long long task = t0; task < t1; ++task) {
+    const int unit = a.fix_units[task / groups];
+    const int c0 = (int)(task % groups) * FIX_COLS;
+    const int nseg = useg(a, unit, G);
+    if (tid == 0) {
+      const int want = nseg * NHW;
+      int spins = 0;
+      while (ld_acquire(a.unit_cnt + unit) < want) {
+        if (++spins > 4) __nanosleep(64);
+      }
+    }
+    epi_bar();
+    const int cg = tid >> 6, t = tid & 63, r = 4 * t, n = unit * UNIT_ROWS + r;
+    const bool whole_qkv = a.post == POST_QKV_ROPE && nseg == 1;
+    // 4 columns per thread (c0 + cg + 2j): every segment's loads in flight, rounds of 4 segments
+    float4 v[FIX_COLS / 2];
+#pragma unroll
+    for (int j = 0; j < FIX_COLS / 2; ++j) v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!whole_qkv) {
+      const float* part = a.ws + (size_t)unit * a.max_segs * BN * UNIT_ROWS + r;
+      for (int s0 = 0; s0 < nseg; s0 += 4) {
+        float4 y[4][FIX_COLS / 2];
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+          for (int j = 0; j < FIX_COLS / 2; ++j) {
+            const int c = c0 + cg + 2 * j;
+            y[s][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (s0 + s < nseg && c < a.m_tok)
+              asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(y[s][j].x), "=f"(y[s][j].y), "=f"(y[s][j].z), "=f"(y[s][j].w)
+                           : "l"(part + ((size_t)(s0 + s) * BN + c) * UNIT_ROWS));
+          }
+#pragma unroll
+        for (int j = 0; j < FIX_COLS / 2; ++j)
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            if (s0 + s < nseg) { v[j].x += y[s][j].x; v[j].y += y[s][j].y; v[j].z += y[s][j].z; v[j].w += y[s][j].w; }
+      }
+    }
+    const bool full4 = n + 3 < a.n_out;
+#pragma unroll
+    for (int j = 0; j < FIX_COLS / 2; ++j) {
+      const int c = c0 + cg + 2 * j;           // warp-uniform
+      const bool col_ok = c < a.m_tok;
+      const size_t row = (size_t)c * a.ld_out;
+      if (a.post == POST_QKV_ROPE) {
+        if (!col_ok) continue;                  // warp-uniform: the shuffles stay convergent
+        float x[4];
+        if (!whole_qkv) {
+          x[0] = __bfloat162float(__float2bfloat16(v[j].x));
+          x[1] = __bfloat162float(__float2bfloat16(v[j].y));
+          x[2] = __bfloat162float(__float2bfloat16(v[j].z));
+          x[3] = __bfloat162float(__float2bfloat16(v[j].w));
+        } else {
+          uint2 q = make_uint2(0u, 0u);
+          if (n < a.n_out) q = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(a.out) + row + n));
+          x[0] = bf16_lo(q.x); x[1] = bf16_hi(q.x); x[2] = bf16_lo(q.y); x[3] = bf16_hi(q.y);
+        }
+        if (ra.hd == 128) qkv_rope_col<128>(a, ra, unit, c, t, lane, x);
+        else qkv_rope_col<64>(a, ra, unit, c, t, lane, x);
+        continue;
+      }
+      if (a.post == POST_RESID_NORM || a.epilogue == EPI_RESID_ADD_F32) {
+        if (col_ok && n < a.n_out) {
+          float* o = reinterpret_cast<float*>(a.out) + row + n;
+          float4 rr = __ldcg(reinterpret_cast<const float4*>(o));
+          rr.x += v[j].x; rr.y += v[j].y; rr.z += v[j].z; rr.w += v[j].w;
+          __stcg(reinterpret_cast<float4*>(o), rr);
+        }
+        continue;
+      }
+      switch (a.epilogue) {
+        case EPI_STORE_BF16: {
+          bf16* o = reinterpret_cast<bf16*>(a.out) + row + n;
+          if (col_ok && full4) {
+            *reinterpret_cast<uint2*>(o) = make_uint2(pack_bf16(v[j].x, v[j].y), pack_bf16(v[j].z, v[j].w));
+          } else if (col_ok) {
+            const float e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+            for (int i = 0; i < 4; ++i)
+              if (n + i < a.n_out) o[i] = __float2bfloat16(e[i]);
+          }
+          break;
+        }
+        case EPI_SILU_MUL: {
+          bf16* o = reinterpret_cast<bf16*>(a.out) + row + (n >> 1);
+          if (col_ok && full4) {
+            *reinterpret_cast<uint32_t*>(o) = pack_bf16(silu(v[j].x) * v[j].y, silu(v[j].z) * v[j].w);
+          } else if (col_ok) {
+            if (n + 1 < a.n_out) o[0] = __float2bfloat16(silu(v[j].x) * v[j].y);
+            if (n + 3 < a.n_out) o[1] = __float2bfloat16(silu(v[j].z) * v[j].w);
+          }
+          break;
+        }
+        case EPI_LOGITS_ARGMAX: {
+          if (!col_ok) break;                   // warp-uniform
+          if (a.out) {
+            float* o = reinterpret_cast<float*>(a.out) + row + n;
+            if (full4) {
+              *reinterpret_cast<float4*>(o) = v[j];
+            } else {
+              const float e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+              for (int i = 0; i < 4; ++i)
+                if (n + i < a.n_out) o[i] = e[i];
+            }
+          }
+          const float e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+          float bv = -INFINITY;
+          int bi = n;
+          for (int i = 0; i < 4; ++i)
+            if (n + i < a.n_out && e[i] > bv) { bv = e[i]; bi = n + i; }
+          warp_argmax(bv, bi);
+          if (lane == 0) {
+            const size_t tile = (size_t)(unit * 2 + (t >> 5)) * a.m_cap + c;
+            a.amax_val[tile] = bv;
+            a.amax_idx[tile] = bi;
+          }
+          break;
+        }
+      }
+    }
+    if (a.post == POST_RESID_NORM)
+      resid_arrive(a, na, 0, c0, min(c0 + FIX_COLS, a.m_tok), 2, slist, red, tid);
+    // task done: the last of the unit's tasks resets its counts for the next launch
+    epi_bar();
+    if (tid == 0 && atom_add_acq_rel(a.unit_cnt + units + unit, 1) + 1 == groups) {
+      a.unit_cnt[unit] = 0;
+      a.unit_cnt[units + unit] = 0;
+    }
+  }
+}
+
+#ifdef PM_GEMM_MAXNREG   // build-time A/B: leave register room for a co-resident fixup CTA
+#define PM_GEMM_BOUNDS __maxnreg__(PM_GEMM_MAXNREG)
+#else
+#define PM_GEMM_BOUNDS __launch_bounds__(NUM_THREADS, 1)
+#endif
+template <int BN, int NH, bool FUSED>
+__global__ void PM_GEMM_BOUNDS
+gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a, NormArgs na, RopeArgs ra) {
   using C = Cfg<BN, NH>;
   constexpr bool PAIR = NH == 1;
   extern __shared__ uint8_t smem_raw[];
@@ -284,6 +636,18 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
           if ((it & 1) != par) continue;
           const int s = it % C::STAGES;
+          if (it == C::STAGES && a.pf_ahead && a.tok_tiles == 1 && crank == 0) {
+            // The ring is full and the MMA is about to wait on the activations (the
+            // previous kernel): keep HBM busy by pulling the worker's next bytes into
+            // L2.  Linear k-block j of the packed weight is bytes [j, j + 1) x 32 KB
+            // (both 128-row halves: in pair mode CTA 0 fetches for both).
+            const unsigned long long b0 = (unsigned long long)(lo + C::STAGES) * A_BYTES;
+            const unsigned long long b1 =
+                min((unsigned long long)hi * A_BYTES, b0 + (unsigned long long)a.pf_ahead * (PAIR ? 2 : 1));
+            for (unsigned long long o = b0; o < b1; o += 32768)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.w + o), "r"((uint32_t)min(32768ull, b1 - o))
+                           : "memory");
+          }
           // both CTAs released the stage (the X multicast overwrites both)
           if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
           mbar_arrive_expect_tx(&full[s], C::STAGE);
@@ -297,8 +661,12 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
       if (a.pf_bytes && par == 0) {
         pdl_wait();
         const unsigned long long share = ((a.pf_bytes / gridDim.x) + 15) & ~15ull;
-        const unsigned long long b0 = share * blockIdx.x;
-        const unsigned long long b1 = min(a.pf_bytes & ~15ull, b0 + share);
+        unsigned long long b0 = share * blockIdx.x;
+        unsigned long long b1 = min(a.pf_bytes & ~15ull, b0 + share);
+        if (a.pf_span) {   // stripes: the first bytes of each next-GEMM worker's range
+          b0 = ((a.pf_span / gridDim.x) * blockIdx.x) & ~15ull;
+          b1 = min(a.pf_span & ~15ull, b0 + share);
+        }
         for (unsigned long long o = b0; o < b1; o += 65536) {
           const uint32_t len = (uint32_t)min(65536ull, b1 - o);
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.pf + o), "r"(len) : "memory");
@@ -422,6 +790,16 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
+      if (FUSED && !(a.debug & 1)) {
+        const int tid = threadIdx.x - EPI_WARP0 * 32;
+        if (!whole || a.post == POST_QKV_ROPE) {
+          // this CTA's part of the unit is stored (partial, or the whole unit's bf16 for the QKV post)
+          epi_bar();
+          if (tid == 0) red_release_add(a.unit_cnt + sg.unit, 1);
+        } else if (a.post == POST_RESID_NORM) {
+          resid_arrive(a, na, tok_base, 0, tok_end, NH, red_idx, red_val, tid);
+        }
+      }
       if (argmax && !(a.debug & 1)) {
         epi_bar();
         // argmax tiles are 128-row halves: this CTA's rows go to tile 2u + crank
@@ -446,6 +824,8 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a) {
       }
     }
   }
+  if (FUSED && !(a.debug & 1) && warp >= EPI_WARP0 && warp < EPI_WARP0 + 4)
+    fused_fixup<BN>(a, na, ra, G, PAIR ? 2 : 1, red_idx, red_val, threadIdx.x - EPI_WARP0 * 32);
   if (threadIdx.x == EPI_WARP0 * 32) PM_TRACE(3);   // epilogue done
   tc_fence_before();
   __syncthreads();
@@ -658,13 +1038,6 @@ __global__ void __launch_bounds__(256) gemm_reduce_v4_kernel(GemmArgs a, int gri
 // RMSNorm of every finished row: the CTA that completes a token row last
 // (per-row arrival count over the split units) normalises it into `xn`.
 // No CTA ever waits, so there is no co-residency assumption.
-struct NormArgs {
-  const bf16* w;      // [d] RMSNorm weight
-  bf16* xn;           // [m_cap][d] normalised output (the next GEMM's TMA source)
-  int* row_cnt;       // [m_cap] arrival counts, zero at rest
-  int n_split;        // units of this launch with > 1 segment (all arrive once per row)
-  float eps;
-};
 
 // RMSNorm of rows x[rows[j]] (fp32, row stride ld) -> y (bf16, row stride
 // d) by the whole CTA (256 threads), one row at a time held in registers:
@@ -845,17 +1218,6 @@ __global__ void __launch_bounds__(256, 4) gemm_resid_norm_v4_kernel(GemmArgs a, 
 // thread = feature.  Split units are summed from the partials, whole units
 // read the bf16 the GEMM epilogue stored; either way the value is rounded to
 // bf16 first (the same rounding the unfused qkv buffer applies).
-struct RopeArgs {
-  bf16* q_out;              // [M][H][hd]
-  bf16* pool;               // block-first KV pool
-  const int* block_table;   // [M][max_blocks]
-  const int* positions;     // [M]
-  const float* rope;        // [pos][hd] cos | sin
-  const bf16* qn_w;         // [hd] or null
-  const bf16* kn_w;
-  int H, Hkv, hd, layer, L_s, max_blocks;
-  float eps;
-};
 
 template <int BN, int RC>
 __global__ void __launch_bounds__(256) gemm_qkv_rope_kernel(GemmArgs a, int grid, RopeArgs ra) {
@@ -1052,8 +1414,6 @@ __global__ void __launch_bounds__(256) gemm_qkv_rope_v4_kernel(GemmArgs a, int g
   *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]));
 }
 
-enum Post : int { POST_NONE = 0, POST_RESID_NORM = 1, POST_QKV_ROPE = 2 };
-
 bool getenv_flag(const char* name) {
   const char* v = getenv(name);
   return v && atoi(v);
@@ -1070,21 +1430,27 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int pos
   using C = Cfg<BN, NH>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_stream_kernel<BN, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_stream_kernel<BN, NH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_stream_kernel<BN, NH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
   cudaError_t e;
+  const NormArgs nav = na ? *na : NormArgs{};
+  const RopeArgs rav = ra ? *ra : RopeArgs{};
+  auto kern = a.fused ? gemm_stream_kernel<BN, NH, true> : gemm_stream_kernel<BN, NH, false>;
   if (NH == 1)   // grid = 2 x workers: each stream-K worker is a (2,1,1) cluster
-    e = launch_k_cluster(gemm_stream_kernel<BN, NH>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, 2, *tx, a);
+    e = launch_k_cluster(kern, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, 2, *tx, a, nav, rav);
   else
-    e = launch_k(gemm_stream_kernel<BN, NH>, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, *tx, a);
+    e = launch_k(kern, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, *tx, a, nav, rav);
   if (e != cudaSuccess) return (int)e;
   if (g_split_event) {
     cudaEventRecord(g_split_event, st);
     g_split_event = nullptr;
   }
+  if (a.fused) return 0;   // the kernel finished every unit itself
   const int G = NH == 1 ? grid / 2 : grid;
   if ((a.debug & 16) || ((a.debug & 32) && post == POST_NONE) || ((a.debug & 64) && post == POST_RESID_NORM) ||
       ((a.debug & 128) && post == POST_QKV_ROPE))
@@ -1154,7 +1520,10 @@ extern "C" int pm_prepare_gemm(void) {
   cudaError_t e = cudaSuccess;
 #define PM_SET(BN, NH)                                                                                    \
   if (e == cudaSuccess)                                                                                   \
-    e = cudaFuncSetAttribute(gemm_stream_kernel<BN, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+    e = cudaFuncSetAttribute(gemm_stream_kernel<BN, NH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             Cfg<BN, NH>::SMEM);                                                          \
+  if (e == cudaSuccess)                                                                                   \
+    e = cudaFuncSetAttribute(gemm_stream_kernel<BN, NH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              Cfg<BN, NH>::SMEM);
   PM_SET(16, 1) PM_SET(32, 1) PM_SET(64, 1) PM_SET(128, 1) PM_SET(256, 1)
   PM_SET(16, 2) PM_SET(32, 2) PM_SET(64, 2) PM_SET(128, 2) PM_SET(256, 2)
@@ -1187,17 +1556,35 @@ extern "C" int pm_gemm_split_units(long long total, int kb, int grid) {
   return n;
 }
 
+// The units a stream-K partition splits (ascending) into out[] (room for
+// total / kb entries); returns the count (the fused fixup's task units).
+extern "C" int pm_gemm_fix_units(long long total, int kb, int grid, int* out) {
+  int n = 0;
+  for (long long u = 0; u * kb < total; ++u) {
+    const long long first = ((u * kb + 1) * grid + total - 1) / total - 1;
+    const long long last = (((u + 1) * kb) * grid + total - 1) / total - 1;
+    if (last > first) out[n++] = (int)u;
+  }
+  return n;
+}
+
 static int make_args(GemmArgs& a, int& grid, int pair, const void* w_packed, int n_out, int n_units, int k,
                      int m_tok, int bn, int epilogue, void* out, int ld_out, float* ws, int max_segs,
                      float* amax_val, int* amax_idx, int m_cap, const void* prefetch,
-                     unsigned long long prefetch_bytes) {
+                     unsigned long long prefetch_bytes, unsigned long long prefetch_span, int* fix_counters,
+                     const int* fix_units, int n_fix) {
   if (k % BK || m_tok < 1 || m_tok > m_cap || grid < (pair ? 2 : 1)) return (int)cudaErrorInvalidValue;
   const int tok_tiles = (m_tok + bn - 1) / bn;
   a = GemmArgs{reinterpret_cast<const uint8_t*>(w_packed), n_out, n_units, k / BK, m_tok, tok_tiles, epilogue,
                out, ld_out, ws, max_segs, amax_val, amax_idx, m_cap,
                reinterpret_cast<const uint8_t*>(prefetch), prefetch ? prefetch_bytes : 0ull,
-               (long long)n_units * tok_tiles * (k / BK), 0};
+               prefetch ? prefetch_span : 0ull, 0u, (long long)n_units * tok_tiles * (k / BK), 0,
+               fix_counters ? 1 : 0, POST_NONE, fix_counters, fix_units, n_fix};
+  // fused fixup: one token tile, 16-byte row quads (the v4 epilogues' layout), a task list
+  if (fix_counters && (tok_tiles != 1 || n_out % 4 || ld_out % 4 || n_fix < 0 || (n_fix && !fix_units)))
+    return (int)cudaErrorInvalidValue;
   if (getenv("PM_GEMM_DEBUG")) a.debug = atoi(getenv("PM_GEMM_DEBUG"));
+  if (getenv("PM_PF_AHEAD_KB")) a.pf_ahead = 1024u * (unsigned)atoi(getenv("PM_PF_AHEAD_KB"));   // A/B
   if (getenv("PM_GEMM_GRID")) grid = atoi(getenv("PM_GEMM_GRID"));  // tuning experiments only
   // grid = CTAs; a worker is one CTA, or a 2-CTA cluster in pair mode; at
   // most one worker per k-block
@@ -1224,10 +1611,12 @@ static int dispatch_bn(int bn, F&& f) {
 extern "C" int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
                        int bn, int grid, int cta_pair, int epilogue, void* out, int ld_out, float* ws, int max_segs,
                        float* amax_val, int* amax_idx, int m_cap, const void* prefetch,
-                       unsigned long long prefetch_bytes, void* stream) {
+                       unsigned long long prefetch_bytes, unsigned long long prefetch_span, int* fix_counters,
+                       const int* fix_units, int n_fix, void* stream) {
   GemmArgs a;
   int rc = make_args(a, grid, cta_pair, w_packed, n_out, n_units, k, m_tok, bn, epilogue, out, ld_out, ws, max_segs,
-                     amax_val, amax_idx, m_cap, prefetch, prefetch_bytes);
+                     amax_val, amax_idx, m_cap, prefetch, prefetch_bytes, prefetch_span, fix_counters, fix_units,
+                     n_fix);
   if (rc) return rc;
   auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   auto st = reinterpret_cast<cudaStream_t>(stream);
@@ -1240,11 +1629,14 @@ extern "C" int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int 
 // stream-K partition splits no unit the norm runs as a separate kernel.
 extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k,
                                      int m_tok, int bn, int grid, int cta_pair, float* resid, float* ws, int max_segs, int m_cap,
-                                     const void* prefetch, unsigned long long prefetch_bytes, const void* norm_w,
-                                     void* xn, float eps, int* row_counters, int split_norm, void* stream) {
+                                     const void* prefetch, unsigned long long prefetch_bytes,
+                                     unsigned long long prefetch_span, const void* norm_w, void* xn, float eps,
+                                     int* row_counters, int split_norm, int* fix_counters, const int* fix_units,
+                                     int n_fix, void* stream) {
   GemmArgs a;
   int rc = make_args(a, grid, cta_pair, w_packed, n_out, n_units, k, m_tok, bn, EPI_RESID_ADD_F32, resid, n_out, ws,
-                     max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes);
+                     max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes, prefetch_span, fix_counters,
+                     fix_units, n_fix);
   if (rc) return rc;
   if (n_out % 8 || n_out > 256 * 4 * NORM_V4) return (int)cudaErrorInvalidValue;
   NormArgs na{reinterpret_cast<const bf16*>(norm_w), reinterpret_cast<bf16*>(xn), row_counters,
@@ -1254,6 +1646,12 @@ extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, i
   // split_norm: finish split units with the plain reduce kernel and normalise in
   // a separate row-parallel kernel (measured better when nothing overlaps the
   // arrival chain: one micro-batch in flight)
+  if (a.fused) {   // residual add and the next norm happen inside the GEMM kernel
+    a.post = POST_RESID_NORM;
+    return dispatch_bn(bn, [&](auto c) {
+      return launch_any<decltype(c)::value>(cta_pair, tx, a, grid, st, POST_RESID_NORM, &na);
+    });
+  }
   const int post = (na.n_split > 0 && !(a.debug & 1) && !split_norm) ? POST_RESID_NORM : POST_NONE;
   rc = dispatch_bn(bn, [&](auto c) { return launch_any<decltype(c)::value>(cta_pair, tx, a, grid, st, post, &na); });
   if (rc || post == POST_RESID_NORM || (a.debug & 16)) return rc;
@@ -1266,13 +1664,17 @@ extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, i
 // scratch for units the partition leaves whole.
 extern "C" int pm_gemm_qkv_rope(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
                                 int bn, int grid, int cta_pair, void* qkv_out, float* ws, int max_segs, int m_cap,
-                                const void* prefetch, unsigned long long prefetch_bytes, void* q_out, void* pool,
+                                const void* prefetch, unsigned long long prefetch_bytes,
+                                unsigned long long prefetch_span, int* fix_counters, const int* fix_units, int n_fix,
+                                void* q_out, void* pool,
                                 const int* block_table, const int* positions, const float* rope, const void* qn_w,
                                 const void* kn_w, int H, int Hkv, int hd, int layer, int L_s, int max_blocks,
                                 float eps, void* stream) {
   GemmArgs a;
   int rc = make_args(a, grid, cta_pair, w_packed, n_out, n_units, k, m_tok, bn, EPI_STORE_BF16, qkv_out, n_out, ws,
-                     max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes);
+                     max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes, prefetch_span, fix_counters,
+                     fix_units, n_fix);
+  if (a.fused) a.post = POST_QKV_ROPE;
   if (rc) return rc;
   if (n_out != (H + 2 * Hkv) * hd || (hd != 64 && hd != 128) || UNIT_ROWS % hd) return (int)cudaErrorInvalidValue;
   RopeArgs ra{reinterpret_cast<bf16*>(q_out), reinterpret_cast<bf16*>(pool), block_table, positions, rope,

@@ -38,6 +38,12 @@ from .scheduler import SchedulerState
 from .stage import StageExecutor
 from .trace import EpisodeMetrics, EventTrace
 
+# single-lane engines finish split-K units inside the GEMM kernels (one launch
+# per projection) with PM_FUSED_FIXUP=1 -- measured slower than the post kernels
+# (c3 stage 2.53 vs 1.94 ms/step, profiles/r2/fused_fixup.md), so opt-in
+import os as _os
+FUSED_FIXUP = _os.environ.get("PM_FUSED_FIXUP", "0") == "1"
+
 
 class _MetaRing:
     """Mapped pinned host staging for per-step metadata (pm_host_alloc);
@@ -143,6 +149,8 @@ class DecodeEngine:
         # chain, and fixup + a row-parallel norm kernel measured faster
         for ex, _ in self.stages:
             ex.split_norm = lanes == 1
+            if lanes == 1 and FUSED_FIXUP:
+                ex.enable_fused()
         self.lane_stages = [self.stages]
         for li in range(1, lanes):
             self.lane_stages.append([(ex.clone_lane(), kv) for ex, kv in self.stages])

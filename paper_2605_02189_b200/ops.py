@@ -256,6 +256,8 @@ class GemmWorkspace:
         self.amax_idx = torch.empty(2 * max(1, vocab_units) * m_cap, dtype=torch.int32, device=device)
         # per-row arrival counts of the fused residual + RMSNorm epilogue; kernels leave them zero
         self.row_cnt = torch.zeros(m_cap, dtype=torch.int32, device=device)
+        # per-unit segment arrivals + finished tasks of the in-kernel fixup (Linear.fused); left zero
+        self.fix_cnt = torch.zeros(2 * max(1, max_units, vocab_units), dtype=torch.int32, device=device)
 
     @staticmethod
     def floats_needed(linears, m_cap):
@@ -280,10 +282,39 @@ class Linear:
         self.sms = None   # SMs the stream-K workers span (None: GEMM_CTAS)
         self._cl = None   # (slices, clusters) of the cluster split-K launch (cl_plan)
         self.cl_ctas = None
+        # in-kernel split-K fixup (single-lane engines, see pm_gemm): the task unit lists
+        self.fused = False
+        self._fix = None
+
+    def enable_fused(self, device):
+        """Finish split units inside the GEMM kernel from now on (one stream of
+        dependent kernels only: the kernel waits on its own CTAs).  Builds the
+        task-unit lists -- the split units, and every unit for the QKV post --
+        which depend on (units, K, workers) only."""
+        import numpy as np
+        bn, grid, segs, tt, pair = self.plan(1)
+        workers = grid // 2 if pair else grid
+        buf = np.zeros(self.n_units, dtype=np.int32)
+        n = _C.lib().pm_gemm_fix_units(C.c_longlong(self.n_units * self.kb), self.kb, workers,
+                                       buf.ctypes.data_as(C.c_void_p))
+        split = torch.from_numpy(buf[:n].copy()).to(device)
+        every = torch.arange(self.n_units, dtype=torch.int32, device=device)
+        self._fix = {False: (split, n), True: (every, self.n_units)}
+        self.fused = True
+
+    def _fixargs(self, m_tok, ws, qkv=False):
+        """(counters, unit list, count) of an in-kernel fixup launch, or nulls
+        (post kernel) when not fused or the step spans several token tiles."""
+        if not self.fused or self.plan(m_tok)[3] != 1:
+            return None, None, 0
+        lst, n = self._fix[qkv]
+        return C.c_void_p(ws.fix_cnt.data_ptr()), C.c_void_p(lst.data_ptr()), n
 
     def launches(self, m_tok) -> int:
         """Kernels one call launches: the stream-K GEMM, plus gemm_reduce when
-        the partition splits units."""
+        the partition splits units (none when the fixup is in-kernel)."""
+        if self.fused and self.plan(m_tok)[3] == 1:
+            return 1
         return 1 + (self.plan(m_tok)[2] > 1)
 
     def plan(self, m_tok):
@@ -294,7 +325,12 @@ class Linear:
 
     @staticmethod
     def _pf(prefetch):
-        return (None, 0) if prefetch is None else (C.c_void_p(prefetch[0].data_ptr()), int(prefetch[1]))
+        """(ptr, bytes, span): prefetch = (tensor, bytes) for the contiguous
+        first bytes, or (tensor, bytes, span) for one stripe per CTA spread
+        over ``span`` bytes (the next GEMM's workers' first k-blocks)."""
+        if prefetch is None:
+            return None, 0, 0
+        return C.c_void_p(prefetch[0].data_ptr()), int(prefetch[1]), int(prefetch[2]) if len(prefetch) > 2 else 0
 
     def _timed(self, kind_bytes, stream, go):
         if TIMER is None:
@@ -307,12 +343,13 @@ class Linear:
         """``prefetch``: optional (tensor, nbytes) the next operation reads
         first; the kernel pulls it into L2 while it drains."""
         bn, grid, segs, tt, pair = self.plan(m_tok)
-        pf_ptr, pf_bytes = self._pf(prefetch)
+        pf_ptr, pf_bytes, pf_span = self._pf(prefetch)
+        fx = self._fixargs(m_tok, ws)
 
         def go():
             _C.call("pm_gemm", _ptr(self.packed), x_maps[bn // 2 if pair else bn].ptr, self.n_out, self.n_units, self.k, m_tok, bn,
                     grid, int(pair), epilogue, _ptr(out), ld_out, _ptr(ws.ws), segs,
-                    _ptr(ws.amax_val), _ptr(ws.amax_idx), ws.m_cap, pf_ptr, pf_bytes, _stream(stream))
+                    _ptr(ws.amax_val), _ptr(ws.amax_idx), ws.m_cap, pf_ptr, pf_bytes, pf_span, *fx, _stream(stream))
         out_b = {EPI_STORE_BF16: 2, EPI_RESID_ADD: 8, EPI_SILU_MUL: 1,
                  EPI_LOGITS_ARGMAX: 4 if out is not None else 0}[epilogue]
         self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * out_b, stream, go)
@@ -322,12 +359,13 @@ class Linear:
         """resid += x W^T, then xn = RMSNorm(resid) * norm_w -- the residual
         projection fused with the next layer norm (pm_gemm_resid_rmsnorm)."""
         bn, grid, segs, tt, pair = self.plan(m_tok)
-        pf_ptr, pf_bytes = self._pf(prefetch)
+        pf_ptr, pf_bytes, pf_span = self._pf(prefetch)
+        fx = self._fixargs(m_tok, ws)
 
         def go():
             _C.call("pm_gemm_resid_rmsnorm", _ptr(self.packed), x_maps[bn // 2 if pair else bn].ptr, self.n_out, self.n_units, self.k,
-                    m_tok, bn, grid, int(pair), _ptr(resid), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, _ptr(norm_w),
-                    _ptr(xn), float(eps), _ptr(ws.row_cnt), int(split_norm), _stream(stream))
+                    m_tok, bn, grid, int(pair), _ptr(resid), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, pf_span, _ptr(norm_w),
+                    _ptr(xn), float(eps), _ptr(ws.row_cnt), int(split_norm), *fx, _stream(stream))
         self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * (8 + 4 + 2), stream, go)
 
     def cl(self, x_maps: dict, m_tok: int, epilogue: int, stream=None, *, m_cap: int, out=None, ld_out=0, rs=None, eps=0.0,
@@ -366,11 +404,12 @@ class Linear:
         """QKV projection fused with q/k RMSNorm + RoPE + paged KV append
         (pm_gemm_qkv_rope); ``qkv`` is scratch for units left whole."""
         bn, grid, segs, tt, pair = self.plan(m_tok)
-        pf_ptr, pf_bytes = self._pf(prefetch)
+        pf_ptr, pf_bytes, pf_span = self._pf(prefetch)
+        fx = self._fixargs(m_tok, ws, qkv=True)
 
         def go():
             _C.call("pm_gemm_qkv_rope", _ptr(self.packed), x_maps[bn // 2 if pair else bn].ptr, self.n_out, self.n_units, self.k,
-                    m_tok, bn, grid, int(pair), _ptr(qkv), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, _ptr(q_out),
+                    m_tok, bn, grid, int(pair), _ptr(qkv), _ptr(ws.ws), segs, ws.m_cap, pf_ptr, pf_bytes, pf_span, *fx, _ptr(q_out),
                     _ptr(pool), _ptr(block_table), _ptr(positions), _ptr(rope), _ptr(qn_w), _ptr(kn_w), H, Hkv,
                     hd, layer, L_s, block_table.shape[1], float(eps), _stream(stream))
         self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * 2, stream, go)

@@ -29,8 +29,19 @@ def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor
     return torch.stack([w_gate, w_up], dim=1).reshape(-1, w_gate.shape[1]).contiguous()
 
 
+# L2 prefetch of the next projection's first weight bytes, issued by each
+# GEMM's producers once their own loads are out (covers the fixup tail);
+# MB per projection, 0 = off.  Single-lane engines only (with two lanes the
+# other lane keeps HBM busy and the extra traffic competes).
+import os as _os
+PF_MB = float(_os.environ.get("PM_PF_MB", "0"))
+PF_QKV = _os.environ.get("PM_PF_QKV", "0") == "1"
+PF_STRIPES = _os.environ.get("PM_PF_STRIPES", "1") == "1"   # stripes at every next-GEMM worker's start   # QKV also prefetches O (across attention)
+
+
 class StageExecutor:
     split_norm = False   # O/down fixup + separate RMSNorm kernel (set by the engine for one lane)
+    fused = False        # split-K fixups inside the GEMM kernels (enable_fused; single-lane engines)
 
     def __init__(self, spec: ModelSpec, layers: range, *, first: bool, last: bool, m_cap: int,
                  pool_blocks: int, max_blocks: int, n_slots: int, device, seed: int = 0,
@@ -117,6 +128,19 @@ class StageExecutor:
                                      max(l.n_units for l in lins), self.lm_head.n_units if self.last else 1, device)
         self.aws = ops.AttnWorkspace(m_cap, s.Hkv, s.hd, self.max_blocks, device, rows_hint=self.rows_hint)
 
+    def enable_fused(self):
+        """Every projection finishes its split units (and its fused epilogue:
+        residual + next RMSNorm, q/k norm + RoPE + KV append, SiLU, logits +
+        argmax) inside its own GEMM kernel -- one launch per projection.  The
+        kernel's fixup tasks wait on other CTAs of the same grid, so this is
+        for engines with ONE stream of dependent kernels (lanes == 1)."""
+        for w in self.W:
+            for k in ("qkv", "o", "gu", "down"):
+                w[k].enable_fused(self.dev)
+        if self.last:
+            self.lm_head.enable_fused(self.dev)
+        self.fused = True
+
     def clone_lane(self) -> "StageExecutor":
         """A second executor over the same weights, KV pool and token table
         with its own activations/metadata/workspaces/graphs, so two
@@ -157,24 +181,33 @@ class StageExecutor:
         # the stage's first norm; every later norm is fused into the residual
         # projection that precedes it (pm_gemm_resid_rmsnorm)
         ops.rmsnorm(self.resid, self.W[0]["attn_norm"], self.xn, M, s.eps, stream)
+        pfb = int(PF_MB * 2**20) if self.split_norm else 0
+
+        def pf(lin):   # (packed weight, bytes) of the projection that streams next
+            if not pfb or lin is None:
+                return None
+            span = lin.packed.numel() * 2 if PF_STRIPES else 0
+            return (lin.packed, min(pfb, lin.weight_bytes), span)
         for li, w in enumerate(self.W):
+            nxt_w = self.W[li + 1] if li + 1 < len(self.W) else None
             # QKV projection + q/k norm + RoPE + paged KV append (one fused epilogue)
             w["qkv"].qkv_rope(self.xn_maps, M, self.qkv, self.gws, self.q, self.pool, self.block_table,
                               self.positions, self.rope, w["q_norm"], w["k_norm"], s.H, s.Hkv, s.hd, li, self.L_s,
-                              s.eps, stream)
+                              s.eps, stream, prefetch=pf(w["o"]) if PF_QKV else None)
             if layer_hook is not None:   # layer li's K/V is in the pool (prefill offload)
                 layer_hook(li)
             ops.paged_attention(self.pool_map, self.q, self.block_table, self.seq_lens, self.attn, self.aws,
                                 M, s.H, s.Hkv, s.hd, li, self.L_s, stream, kv_tokens=kv_tokens)
             # O projection + residual + post-attention RMSNorm
             w["o"].resid_rmsnorm(self.attn_maps, M, self.resid, self.gws, w["mlp_norm"], self.xn, s.eps, stream,
-                                 split_norm=self.split_norm)
-            w["gu"](self.xn_maps, M, ops.EPI_SILU_MUL, self.act, s.ffn, self.gws, stream)
+                                 split_norm=self.split_norm, prefetch=pf(w["gu"]))
+            w["gu"](self.xn_maps, M, ops.EPI_SILU_MUL, self.act, s.ffn, self.gws, stream, prefetch=pf(w["down"]))
             # down projection + residual + the next norm (next layer's, or the final one)
             nxt = self.W[li + 1]["attn_norm"] if li + 1 < len(self.W) else (self.final_norm if self.last else None)
+            nxt_lin = nxt_w["qkv"] if nxt_w is not None else (self.lm_head if self.last else None)
             if nxt is not None:
                 w["down"].resid_rmsnorm(self.act_maps, M, self.resid, self.gws, nxt, self.xn, s.eps, stream,
-                                        split_norm=self.split_norm)
+                                        split_norm=self.split_norm, prefetch=pf(nxt_lin))
             else:
                 w["down"](self.act_maps, M, ops.EPI_RESID_ADD, self.resid, s.d, self.gws, stream)
         if self.last:
@@ -248,6 +281,9 @@ class StageExecutor:
         M = M or self.m_cap
         if ops.CL_GEMM and M <= ops.CL_MAX_M:
             return (1 if self.first else 0) + 1 + 5 * self.L_s + (2 if self.last else 0)
+        if self.fused and M <= 256:   # one launch per projection + attention
+            n = (1 if self.first else 0) + 1 + 5 * self.L_s
+            return n + (2 if self.last else 0)
         n = (1 if self.first else 0) + 1 + self.L_s * (2 + 1 + 2 + 2)
         if self.split_norm:   # O / down: GEMM + reduce + a separate RMSNorm when the plan splits units
             n += sum((w["o"].launches(M) > 1) + (w["down"].launches(M) > 1) for w in self.W)

@@ -12,6 +12,7 @@ from paper_2605_02189_b200 import _C, ops  # noqa: E402
 from paper_2605_02189_b200.models import LLAMA3_70B, QWEN3_8B, QWEN3_32B  # noqa: E402
 
 dev = "cuda"
+BPCS = (8, 12, 16, 20, 24, 32)
 _C.call("pm_prepare_attention")
 out_f = open(sys.argv[1], "w") if len(sys.argv) > 1 else None
 
@@ -46,7 +47,7 @@ for name, spec, L_s, M, seq in shapes:
     ref = None
     res = []
     for cfg in (1, 2, 0):
-        for bpc in (3, 4, 6, 8, 12, 16):
+        for bpc in BPCS:
             aws = ops.AttnWorkspace(M, Hkv, hd, max_blocks, dev, cfg=cfg)
             aws.bpc = bpc
             aws.max_chunks = max(1, -(-max_blocks // bpc))
