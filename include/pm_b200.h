@@ -50,6 +50,11 @@ int pm_host_device_ptr(void* host, void** dev);
  * kernel on `stream` instead of a copy-engine DMA so it never queues behind KV prefetch copies */
 int pm_meta_upload(int count, void* const* dst, const void* const* src, const int* n, void* stream);
 /* dst_base+dst_off[i] <- src_base+src_off[i], `bytes` each; contiguous runs merged */
+/* decode offload in one DMA: gather the n rows (pool + pool_off[i], `bytes` each) into dev_stage, one
+ * cudaMemcpyAsync to pinned host_stage, then a host function in stream order scatters them to
+ * replica + rep_off[i] (pipeline_sim.py:486-490's eager offload); rep_off / pool_off are host arrays */
+int pm_offload_gather(void* replica, const void* pool, const long long* rep_off, const long long* pool_off, int n,
+                      unsigned long long bytes, void* dev_stage, void* host_stage, void* stream);
 int pm_copy_pieces(void* dst_base, const void* src_base, const long long* dst_off, const long long* src_off,
                    int n, unsigned long long bytes, void* stream);
 

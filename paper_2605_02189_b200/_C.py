@@ -28,6 +28,7 @@ _SIGS = {
     "pm_host_device_ptr": [_P, C.POINTER(_P)],
     "pm_meta_upload": [_I, _P, _P, _P, _P],
     "pm_copy_pieces": [_P, _P, _P, _P, _I, _U64, _P],
+    "pm_offload_gather": [_P, _P, _P, _P, _I, _U64, _P, _P, _P],
     "pm_copy_2d": [_P, _U64, _P, _U64, _U64, _U64, _P],
     "pm_gemm": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _P, _I, _P, _U64, _U64, _P, _P, _I, _P],
     "pm_gemm_resid_rmsnorm": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _I, _I, _P, _U64, _U64, _P, _P, _F, _P, _I, _P, _P, _I, _P],

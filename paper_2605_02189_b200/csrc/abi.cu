@@ -2,11 +2,13 @@
 // host memory, batched KV block copies for the offload engine.
 #include <cudaTypedefs.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include <sys/mman.h>
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -201,6 +203,88 @@ extern "C" int pm_offload_rows(void* host_dev, const void* pool, const void* off
       static_cast<uint8_t*>(host_dev), static_cast<const uint8_t*>(pool), static_cast<const long long*>(offs), n,
       bytes);
   return (int)cudaGetLastError();
+}
+
+// Decode offload in one DMA (REF pipeline_sim.py:486-490).  Each row's new-
+// token KV is one contiguous `bytes` run of the block-first pool; the rows of
+// a step land at scattered host-replica offsets.  Instead of one small DMA per
+// row, a gather kernel packs the rows into a device staging slab, ONE
+// cudaMemcpyAsync moves the slab to pinned host staging, and a host function
+// enqueued behind it (cudaLaunchHostFunc, stream order) scatters the rows into
+// the replica -- so an event recorded on `stream` afterwards means "replica
+// complete", exactly like the per-row copies.  Offsets travel by value.
+namespace {
+constexpr int GATHER_MAX = 2048;
+struct GatherRows {
+  long long pool_off[GATHER_MAX];
+};
+__global__ void __launch_bounds__(256) gather_rows_kernel(uint8_t* __restrict__ stage, const uint8_t* __restrict__ pool,
+                                                          const __grid_constant__ GatherRows g, int n,
+                                                          unsigned long long bytes) {
+  const unsigned long long per_row = bytes / 16, total = per_row * (unsigned long long)n;
+  for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < total; i += gridDim.x * 256ull) {
+    const int row = (int)(i / per_row);
+    const unsigned long long c = (i - row * per_row) * 16;
+    *reinterpret_cast<uint4*>(stage + row * bytes + c) = __ldcs(reinterpret_cast<const uint4*>(pool + g.pool_off[row] + c));
+  }
+}
+struct ScatterCtx {
+  uint8_t* replica;
+  const uint8_t* stage;
+  unsigned long long bytes;
+  int n;
+  long long rep_off[1];   // n entries
+};
+// Host scatter of the staged rows.  One host thread copies ~6-8 GB/s between
+// pinned buffers, so large steps are split over a few threads (no CUDA calls
+// inside a host function).
+void CUDART_CB scatter_rows(void* p) {
+  ScatterCtx* c = static_cast<ScatterCtx*>(p);
+  const size_t total = (size_t)c->n * c->bytes;
+  const int nt = total >= (8u << 20) ? 4 : (total >= (2u << 20) ? 2 : 1);
+  auto part = [c, nt](int t) {
+    for (int i = t; i < c->n; i += nt) memcpy(c->replica + c->rep_off[i], c->stage + (size_t)i * c->bytes, c->bytes);
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(part, t);
+  part(0);
+  for (auto& x : th) x.join();
+  free(c);
+}
+}  // namespace
+
+// replica: host address of the pinned replica; rep_off/pool_off: host arrays
+// of n byte offsets; dev_stage / host_stage: n * bytes of device memory /
+// pinned host memory, not reused until this call's work on `stream` is done
+// (stream order).  bytes % 16 == 0.
+extern "C" int pm_offload_gather(void* replica, const void* pool, const long long* rep_off, const long long* pool_off,
+                                 int n, unsigned long long bytes, void* dev_stage, void* host_stage, void* stream) {
+  if (bytes % 16 || n < 0) return (int)cudaErrorInvalidValue;
+  if (n == 0) return 0;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  for (int r0 = 0; r0 < n; r0 += GATHER_MAX) {
+    const int k = n - r0 < GATHER_MAX ? n - r0 : GATHER_MAX;
+    GatherRows g;
+    for (int i = 0; i < k; ++i) g.pool_off[i] = pool_off[r0 + i];
+    const unsigned long long chunks = bytes / 16 * (unsigned long long)k;
+    const int grid = (int)((chunks + 255) / 256 < 296 ? (chunks + 255) / 256 : 296);
+    gather_rows_kernel<<<grid, 256, 0, st>>>(static_cast<uint8_t*>(dev_stage) + (size_t)r0 * bytes,
+                                             static_cast<const uint8_t*>(pool), g, k, bytes);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return (int)e;
+  }
+  cudaError_t e = cudaMemcpyAsync(host_stage, dev_stage, (size_t)n * bytes, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return (int)e;
+  ScatterCtx* c = static_cast<ScatterCtx*>(malloc(sizeof(ScatterCtx) + sizeof(long long) * (size_t)n));
+  if (!c) return (int)cudaErrorMemoryAllocation;
+  c->replica = static_cast<uint8_t*>(replica);
+  c->stage = static_cast<const uint8_t*>(host_stage);
+  c->bytes = bytes;
+  c->n = n;
+  memcpy(c->rep_off, rep_off, sizeof(long long) * (size_t)n);
+  e = cudaLaunchHostFunc(st, scatter_rows, c);
+  if (e != cudaSuccess) free(c);
+  return (int)e;
 }
 
 // Batched copies of equal-sized KV pieces between two base addresses:

@@ -23,6 +23,7 @@
 // chunk partials (O, m, l) go to a workspace and the last warp to finish a
 // (request, kv head) merges them in chunk order -- chunk boundaries depend
 // only on the request's own length, so results are batch-invariant.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -424,16 +425,20 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
 }
 
 int num_sms();
+int attn_debug();
 
 template <int HD, int WARPS, int STAGES>
 int launch_cfg(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
   using C = AttnCfg<HD, WARPS, STAGES>;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {false};   // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(paged_attn_kernel<HD, WARPS, STAGES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return (int)e;
-    attr = true;
+    attr[dev] = true;
   }
   const int sms = num_sms();
   const long long items = (long long)a.M * a.Hkv * a.max_chunks;
@@ -453,15 +458,27 @@ int attn_cfg() {
   }
   return g_attn_cfg;
 }
-int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (getenv("PM_ATTN_SMS")) sms = atoi(getenv("PM_ATTN_SMS"));   // tuning experiments only
+int num_sms() {   // of the current device (cached per device)
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!sms[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (const char* e = getenv("PM_ATTN_SMS")) n = atoi(e);   // tuning experiments only
+    sms[dev] = n;
   }
-  return sms;
+  return sms[dev];
+}
+int attn_debug() {   // PM_ATTN_DEBUG, read once (profiling only: bit0 gives WRONG results)
+  static const int d = [] {
+    const char* e = getenv("PM_ATTN_DEBUG");
+    const int v = e ? atoi(e) : 0;
+    if (v & 1) fprintf(stderr, "libpmb200: PM_ATTN_DEBUG=%d is a profiling mode -- attention results are NOT valid\n", v);
+    return v;
+  }();
+  return d;
 }
 template <int HD, int WARPS, int STAGES>
 int workers_cfg() {
@@ -507,7 +524,7 @@ extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int*
   if (max_chunks * blocks_per_chunk < max_blocks || blocks_per_chunk > MAX_BPC) return (int)cudaErrorInvalidValue;
   AttnArgs a{reinterpret_cast<const bf16*>(q), block_table, seq_lens, reinterpret_cast<bf16*>(out),
              ws_o, ws_ml, counters, work, M, H, Hkv, G, layer, max_blocks, max_chunks, blocks_per_chunk,
-             1.4426950408889634f / sqrtf((float)hd), getenv("PM_ATTN_DEBUG") ? atoi(getenv("PM_ATTN_DEBUG")) : 0};
+             1.4426950408889634f / sqrtf((float)hd), attn_debug()};
   auto tm = reinterpret_cast<const CUtensorMap*>(tmap_kv);
   auto st = reinterpret_cast<cudaStream_t>(stream);
   if (hd == 128) return launch_attn<128>(tm, a, st, cfg);

@@ -28,6 +28,7 @@
 //     epilogue of one segment overlaps the mainloop of the next.
 // Epilogues: bf16 store, fp32 residual add, SiLU(gate)*up over interleaved
 // gate/up rows, fp32 logits + per-unit argmax partials.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <type_traits>
@@ -1428,14 +1429,17 @@ template <int BN, int NH>
 int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int post, const NormArgs* na,
            const RopeArgs* ra) {
   using C = Cfg<BN, NH>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[64] = {false};   // per device (the attribute is per-context)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(gemm_stream_kernel<BN, NH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::SMEM);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_stream_kernel<BN, NH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return (int)e;
-    attr_set = true;
+    attr_set[dev] = true;
   }
   cudaError_t e;
   const NormArgs nav = na ? *na : NormArgs{};
@@ -1556,6 +1560,25 @@ extern "C" int pm_gemm_split_units(long long total, int kb, int grid) {
   return n;
 }
 
+// Profiling / tuning switches, read once per process (never per launch).
+struct Knobs {
+  int debug;            // PM_GEMM_DEBUG: profiling bits (most give WRONG numerics; warned once)
+  int grid;             // PM_GEMM_GRID: CTA count override (experiments)
+  unsigned pf_ahead;    // PM_PF_AHEAD_KB: L2 run-ahead per CTA (A/B, off)
+};
+static const Knobs& knobs() {
+  static const Knobs k = [] {
+    Knobs r{0, 0, 0u};
+    if (const char* e = getenv("PM_GEMM_DEBUG")) r.debug = atoi(e);
+    if (const char* e = getenv("PM_GEMM_GRID")) r.grid = atoi(e);
+    if (const char* e = getenv("PM_PF_AHEAD_KB")) r.pf_ahead = 1024u * (unsigned)atoi(e);
+    if (r.debug & ~8)
+      fprintf(stderr, "libpmb200: PM_GEMM_DEBUG=%d is a profiling mode -- GEMM results are NOT valid\n", r.debug);
+    return r;
+  }();
+  return k;
+}
+
 // The units a stream-K partition splits (ascending) into out[] (room for
 // total / kb entries); returns the count (the fused fixup's task units).
 extern "C" int pm_gemm_fix_units(long long total, int kb, int grid, int* out) {
@@ -1583,9 +1606,10 @@ static int make_args(GemmArgs& a, int& grid, int pair, const void* w_packed, int
   // fused fixup: one token tile, 16-byte row quads (the v4 epilogues' layout), a task list
   if (fix_counters && (tok_tiles != 1 || n_out % 4 || ld_out % 4 || n_fix < 0 || (n_fix && !fix_units)))
     return (int)cudaErrorInvalidValue;
-  if (getenv("PM_GEMM_DEBUG")) a.debug = atoi(getenv("PM_GEMM_DEBUG"));
-  if (getenv("PM_PF_AHEAD_KB")) a.pf_ahead = 1024u * (unsigned)atoi(getenv("PM_PF_AHEAD_KB"));   // A/B
-  if (getenv("PM_GEMM_GRID")) grid = atoi(getenv("PM_GEMM_GRID"));  // tuning experiments only
+  const Knobs& kn = knobs();
+  a.debug = kn.debug;
+  a.pf_ahead = kn.pf_ahead;
+  if (kn.grid > 0) grid = kn.grid;   // tuning experiments only
   // grid = CTAs; a worker is one CTA, or a 2-CTA cluster in pair mode; at
   // most one worker per k-block
   long long workers = pair ? grid / 2 : grid;

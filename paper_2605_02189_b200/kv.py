@@ -17,10 +17,12 @@ Replaces the reference's simulated links (REF = reference
   prefetched requests' host copy; the step that first executes them waits on
   it (the stall the reference models at pipeline_sim.py:410-421).
 * Offload (step t): the new token's whole-stage KV (one contiguous slot per
-  row) HBM->host on the D2H copy-engine stream right after the step's
-  compute, one cudaMemcpyAsync per run of contiguous rows (pm_copy_pieces,
-  submitted from C).
-  PM_OFFLOAD_DMA=0 selects the SM-side variant (pm_offload_rows: a kernel
+  row) HBM->host on the D2H stream right after the step's compute: a gather
+  kernel packs the rows into a staging slab, ONE cudaMemcpyAsync moves it to
+  pinned host staging and a host function in stream order scatters the rows
+  into the replica (pm_offload_gather).  PM_OFFLOAD_MODE=dma: one
+  cudaMemcpyAsync per run of contiguous rows (pm_copy_pieces).
+  PM_OFFLOAD_MODE=kernel selects the SM-side variant (pm_offload_rows: a kernel
   storing through the mapped replica) for A/B only -- measured at ~1 GB/s
   on B200 (SM stores to mapped host memory), which made C2 4x slower
   (profiles/r2/offload_ab.md).
@@ -36,8 +38,19 @@ import torch
 
 from . import _C
 
-OFFLOAD_DMA = os.environ.get("PM_OFFLOAD_DMA", "1") == "1"
+# decode offload path: "auto" (below), "gather" (pm_offload_gather: gather kernel -> one DMA ->
+# host scatter in stream order), "dma" (pm_copy_pieces: one cudaMemcpyAsync per
+# run of contiguous rows), "kernel" (pm_offload_rows, SM stores through the
+# mapped replica: ~1 GB/s, A/B only)
+OFFLOAD_MODE = os.environ.get("PM_OFFLOAD_MODE", "auto")
+# auto: gather when a step offloads at least this much (C2: 18 MB/step -> gather,
+# 10.4 vs 9.4 GB/s effective; a C3 stage: 1.5 MB/step -> per-row DMAs, where the
+# host function's dispatch latency outweighs the saved copy setups)
+GATHER_MIN_BYTES = 8 << 20
+if os.environ.get("PM_OFFLOAD_DMA") == "0":
+    OFFLOAD_MODE = "kernel"
 OFFLOAD_CTAS = int(os.environ.get("PM_OFFLOAD_CTAS", "32"))
+STAGE_RING = 4   # gather-offload staging slabs (steps in flight on the D2H stream)
 
 
 def device_numa_node(device=None) -> int:
@@ -125,6 +138,8 @@ class KvEngine:
         # older toucher on lane B is not masked by a newer one on lane A.
         self.block_last_compute = [np.full(executor.pool_blocks, -1, dtype=np.int64)]
         self._off_ring = None       # mapped pinned (host, pool) offset pairs of the offload kernel
+        self._stage = None          # gather offload: [STAGE_RING] (device slab, pinned host slab)
+        self._stage_i = 0
 
     def _offsets(self, n: int):
         """A mapped pinned int64 [n][2] buffer for this step's offload offsets
@@ -146,10 +161,27 @@ class KvEngine:
         if slot[2] is not None:
             slot[2].synchronize()
         return slot
+    def _stage_slot(self):
+        """(device slab, pinned host slab) of the gather offload, m_cap rows
+        each; slots rotate and are reused in D2H-stream order only."""
+        if self._stage is None:
+            nb = self.ex.m_cap * self.tok_bytes
+            self._stage = []
+            for _ in range(STAGE_RING):
+                d = torch.empty(nb, dtype=torch.uint8, device=self.dev)
+                p = _C.C.c_void_p()
+                _C.call("pm_host_alloc", nb, _C.C.byref(p))
+                self._stage.append((d, p.value))
+        slot = self._stage[self._stage_i % STAGE_RING]
+        self._stage_i += 1
+        return slot
+
     def __del__(self):
         try:
             for slot in self._off_ring or ():
                 _C.call("pm_host_free", _C.C.c_void_p(slot[3]))
+            for _, hp in self._stage or ():
+                _C.call("pm_host_free", _C.C.c_void_p(hp))
         except Exception:
             pass
 
@@ -303,7 +335,17 @@ class KvEngine:
             if self.timing:
                 rec["d2h_start"] = self._event()
                 rec["d2h_start"].record(s)
-            if OFFLOAD_DMA:
+            mode = OFFLOAD_MODE
+            if mode == "auto":   # one gathered DMA pays off for big steps; per-row DMAs for small ones
+                mode = "gather" if len(rows) * tb >= GATHER_MIN_BYTES else "dma"
+            if mode == "gather":
+                d = np.asarray(dst, dtype=np.int64)
+                sr = np.asarray(src, dtype=np.int64)
+                dslab, hslab = self._stage_slot()
+                _C.call("pm_offload_gather", _C.C.c_void_p(self.rep.ptr), _C.C.c_void_p(self.pool_ptr),
+                        d.ctypes.data_as(_C.C.c_void_p), sr.ctypes.data_as(_C.C.c_void_p), len(rows), tb,
+                        _C.C.c_void_p(dslab.data_ptr()), _C.C.c_void_p(hslab), _C.C.c_void_p(s.cuda_stream))
+            elif mode == "dma":
                 d = np.asarray(dst, dtype=np.int64)
                 sr = np.asarray(src, dtype=np.int64)
                 _C.call("pm_copy_pieces", _C.C.c_void_p(self.rep.ptr), _C.C.c_void_p(self.pool_ptr),
