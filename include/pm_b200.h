@@ -116,15 +116,18 @@ int pm_qkv_rope_append(const void* qkv, void* q_out, void* pool, const int* bloc
 int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_table, const int* seq_lens,
                        const int* work, void* out, float* ws_o, float* ws_ml, int* counters, int M, int H,
                        int Hkv, int hd,
-                       int layer, int L_s, int max_blocks, int max_chunks, int blocks_per_chunk, int cfg,
+                       int layer, int L_s, int max_blocks, int max_chunks, int max_piece, int cfg,
                        void* stream);
 /* cfg: warps x KV-ring stages per SM (0: 6x4, 1: 12x2, 2: 8x3, 3: 4x2 at 2 CTAs/SM; -1: default);
- * the work list must be built for pm_attn_workers_cfg(hd, cfg) warps.  Results do not depend on it. */
-int pm_attn_blocks_per_split(void);
-/* host: a step's attention work list -- non-empty (chunk, row) pairs chunk-major, stably sorted by size
- * descending, odd rounds of workers/hkv entries reversed; work[0] = count, entry j = {(chunk << 16) | row,
- * seq_len} at work[2 + 2j]; work holds 2 + 2 * M * ceil(max_blocks / blocks_per_chunk) ints */
-int pm_attn_work_list(const int* seq_lens, int M, int blocks_per_chunk, int hkv, int workers, int* work);
+ * the work list must be built for pm_attn_workers_cfg(hd, cfg) warps and pieces of at most max_piece
+ * (<= pm_attn_max_piece()) blocks; max_chunks >= the most pieces of one (row, kv head). */
+int pm_attn_max_piece(void);
+/* host: a step's balanced attention work list -- every (row, kv head)'s KV blocks end to end, one equal
+ * range per warp (at least minq blocks), cut into pieces of at most maxp blocks; work[0] = warps used,
+ * work[1] = pieces, work[2 + w] = warp w's first piece, pieces (4 ints: row | kvh << 16, b0 | nblk << 16,
+ * chunk | nchunks << 16, seq_len) from int (3 + used + 3) & ~3.  Returns the ints written (negative
+ * cudaError_t when `cap` is too small). */
+int pm_attn_work_list(const int* seq_lens, int M, int hkv, int workers, int maxp, int minq, int cap, int* work);
 /* warps of a full attention launch on the current device (the `workers` above) */
 int pm_attn_workers(int hd);
 int pm_attn_workers_cfg(int hd, int cfg);

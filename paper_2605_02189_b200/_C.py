@@ -43,10 +43,10 @@ _SIGS = {
     "pm_qkv_rope_append": [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P],
     "pm_argmax_reduce": [_P, _P, _I, _I, _I, _P, _P, _P, _P],
     "pm_paged_attention": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _P],
-    "pm_attn_work_list": [_P, _I, _I, _I, _I, _P],
+    "pm_attn_work_list": [_P, _I, _I, _I, _I, _I, _I, _P],
     "pm_attn_workers": [_I],
     "pm_attn_workers_cfg": [_I, _I],
-    "pm_attn_blocks_per_split": [],
+    "pm_attn_max_piece": [],
     "pm_prepare_gemm": [],
     "pm_prepare_attention": [],
     "pm_hop_pack": [_P, _P, _LL, _P],

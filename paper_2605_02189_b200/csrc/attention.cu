@@ -2,27 +2,25 @@
 // per request).  HBM-bound: every KV byte of the active micro-batch is read
 // exactly once per layer, so the kernel is built to keep every SM streaming.
 //
-// Work item = (request row, kv head, chunk of `bpc` 16-token KV blocks).  The
-// host lists the non-empty (chunk, row) pairs chunk-major (all first chunks,
-// then all second chunks, ...) once per step; item i of the launch is list
-// entry i / Hkv, kv head i % Hkv.  Full-size chunks therefore come first and
-// the ragged tails last, so the static round-robin over warps is balanced.
-// Persistent grid; every WARP is an independent worker that walks its share
-// of the items with its own STAGES-deep TMA pipeline that runs straight
-// across item boundaries (no CTA-wide barriers on the hot path):
+// Work split (host-built, pm_attn_work_list): the KV blocks of every (request
+// row, kv head) unit are laid end to end and cut into one contiguous range of
+// equal length per warp, each range into pieces of at most `maxp` blocks.
+// Every warp therefore streams the same number of KV blocks whatever the rows'
+// lengths (the previous fixed-size chunks left the busiest warp ~1.5x the
+// mean).  Persistent grid; every WARP is an independent worker that walks its
+// pieces with its own STAGES-deep TMA pipeline running straight across piece
+// boundaries (no CTA-wide barriers on the hot path):
 //   lane 0 issues, per KV block, four 128B-swizzled 2-D TMA boxes (K and V,
-//   two 64-dim halves each) and, for the first block of an item, a bulk copy
-//   of the item's GQA query group; the warp consumes them with ldmatrix +
+//   two 64-dim halves each); the warp consumes them with ldmatrix +
 //   mma.sync.m16n8k16 in the transposed arrangement
 //       S^T[16 tok x 8 heads] = K[16 x hd] . Q^T[hd x 8]
 //       O^T[hd x 8 heads]   += V^T[hd x 16] . P^T[16 x 8]
 //   (the 8 q-heads of a GQA group are the MMA N; P^T moves from the S
 //   accumulator to the B fragment with one movmatrix.trans per 8x8), online
 //   softmax in fp32 with warp shuffles.
-// A request with one chunk is normalised and stored by its warp; otherwise
-// chunk partials (O, m, l) go to a workspace and the last warp to finish a
-// (request, kv head) merges them in chunk order -- chunk boundaries depend
-// only on the request's own length, so results are batch-invariant.
+// A unit covered by one piece is normalised and stored by its warp; otherwise
+// piece partials (O, m, l) go to a workspace and the last warp to finish a
+// unit merges them in piece order (deterministic for a given step).
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -34,7 +32,7 @@
 namespace {
 
 constexpr int MAX_G = 8;
-constexpr int MAX_BPC = 32;   // KV blocks per work item (pm_attn_blocks_per_split)
+constexpr int MAX_P = 32;     // KV blocks per piece at most (host ATTN_MAXP)
 
 PM_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -70,8 +68,9 @@ struct AttnArgs {
   float* ws_o;             // [M][Hkv][max_chunks][8][HD]
   float* ws_ml;            // [M][Hkv][max_chunks][2][8]
   int* counters;           // [M][Hkv] merge counts, zero at rest
-  const int* work;         // [0] = #entries, [2 + 2j] = (chunk << 16) | row, [3 + 2j] = seq len; chunk-major
-  int M, H, Hkv, G, layer, max_blocks, max_chunks, bpc;
+  const int* work;         // [0] warps used, [1] pieces, [2 + w] warp w's first piece, pieces (int4) from
+                           // the next 16-byte boundary: (row | kvh << 16, b0 | nblk << 16, chunk | nchunks << 16, seq)
+  int M, H, Hkv, G, layer, max_blocks, max_chunks, maxp;
   float scale_log2;        // log2(e)/sqrt(hd)
   int debug;               // profiling only: bit0 skip the math (memory pipeline alone), bit2 trace
 };
@@ -82,28 +81,29 @@ PM_DEV unsigned long long gtimer() {
   return t;
 }
 
-// A warp's items are gw, gw + W, gw + 2W, ... (W = warps in the grid).  Their
-// descriptors and KV block ids are loaded into the warp's shared memory in
-// windows of up to ITEM_WIN items, all loads in flight at once and before
-// griddepcontrol.wait (the host wrote them), so the streaming loop never
-// waits on metadata.
-constexpr int ITEM_WIN = 32;
-constexpr int WIN_IDS = 256;   // block-id slots per warp window
+// A warp's pieces are work entries [off[gw], off[gw + 1]).  Their descriptors
+// and KV block ids are loaded into the warp's shared memory in windows of up
+// to ITEM_WIN pieces (maxp block-id slots each), all loads in flight at once
+// and before griddepcontrol.wait (the host wrote them), so the streaming loop
+// never waits on metadata.
+constexpr int ITEM_WIN = 8;
+constexpr int WIN_IDS = ITEM_WIN * MAX_P;   // block-id slots per warp window
 
 struct Cursor {
-  int j, blk, nblk, r, kvh, chunk, b0, seq;  // j = item index in the window; b0 = first block
+  int j, blk, nblk, r, kvh, chunk, nchunks, b0, seq;  // j = piece index in the window; b0 = first block
 };
 
 PM_DEV bool item_setup(const AttnArgs& a, const int4* itm, int j, int nw, Cursor& c) {
   if (j >= nw) return false;
-  const int4 m = itm[j];   // (row, first block, kv head, seq len)
+  const int4 m = itm[j];
   c.j = j;
-  c.r = m.x;
-  c.b0 = m.y;
-  c.kvh = m.z;
+  c.r = m.x & 0xffff;
+  c.kvh = (int)((unsigned)m.x >> 16);
+  c.b0 = m.y & 0xffff;
+  c.nblk = (int)((unsigned)m.y >> 16);
+  c.chunk = m.z & 0xffff;
+  c.nchunks = (int)((unsigned)m.z >> 16);
   c.seq = m.w;
-  c.chunk = m.y / a.bpc;
-  c.nblk = min(a.bpc, ((c.seq + 15) >> 4) - c.b0);
   c.blk = 0;
   return true;
 }
@@ -163,8 +163,12 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
     fence_barrier_init();
   }
   __syncwarp();
-  const int n_items = __ldg(&a.work[0]) * a.Hkv;   // host-written: readable before the wait
-  const int win = min(ITEM_WIN, WIN_IDS / a.bpc);
+  // host-written metadata: readable before the wait
+  const int w_used = __ldg(&a.work[0]);
+  const int p_first = gw < w_used ? __ldg(&a.work[2 + gw]) : 0;
+  const int n_items = gw < w_used ? __ldg(&a.work[3 + gw]) - p_first : 0;
+  const int4* pieces = reinterpret_cast<const int4*>(a.work + ((3 + w_used + 3) & ~3)) + p_first;
+  const int win = ITEM_WIN;
 
   const int g8 = lane >> 2, t = lane & 3;
   // per-lane ldmatrix offsets inside a (swizzled) K tile and V tile
@@ -182,22 +186,16 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
   }
   int issued = 0, consumed = 0;
   bool waited = false;
-  for (int j0 = 0;; j0 += win) {
-    const int first = gw + j0 * W;
-    if (first >= n_items) break;
-    const int nw = min(win, (n_items - first + W - 1) / W);
+  for (int j0 = 0; j0 < n_items; j0 += win) {
+    const int nw = min(win, n_items - j0);
     // ---- window metadata: descriptors, then every block id, all in flight
-    if (lane < nw) {
-      const int it = first + lane * W;
-      const int2 e = __ldg(reinterpret_cast<const int2*>(a.work) + 1 + it / a.Hkv);
-      itm[lane] = make_int4(e.x & 0xffff, (e.x >> 16) * a.bpc, it % a.Hkv, e.y);
-    }
+    if (lane < nw) itm[lane] = __ldg(pieces + j0 + lane);
     __syncwarp();
-    for (int idx = lane; idx < nw * a.bpc; idx += 32) {
-      const int4 m = itm[idx / a.bpc];
-      const int k = idx % a.bpc;
-      const int nb = ((m.w + 15) >> 4) - m.y;
-      bid[idx] = k < nb ? __ldg(&a.block_table[(size_t)m.x * a.max_blocks + m.y + k]) : 0;
+    for (int idx = lane; idx < nw * MAX_P; idx += 32) {
+      const int4 m = itm[idx / MAX_P];
+      const int k = idx % MAX_P;
+      const int row = m.x & 0xffff, b0 = m.y & 0xffff, nb = (int)((unsigned)m.y >> 16);
+      bid[idx] = k < nb ? __ldg(&a.block_table[(size_t)row * a.max_blocks + b0 + k]) : 0;
     }
     __syncwarp();
     if (!waited) {
@@ -211,7 +209,7 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
     auto issue_one = [&]() {  // lane 0
       const int s = issued % STAGES;
       uint8_t* dst = wbuf + s * C::STAGE;
-      const int phys = bid[pc.j * a.bpc + pc.blk];
+      const int phys = bid[pc.j * MAX_P + pc.blk];
       const int col_k = ((a.layer * 2 + 0) * a.Hkv + pc.kvh) * HD;
       const int col_v = ((a.layer * 2 + 1) * a.Hkv + pc.kvh) * HD;
       const uint64_t pol = policy_evict_first();
@@ -316,7 +314,7 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
       l1 += __shfl_xor_sync(0xffffffffu, l1, off);
     }
     const int r = cc.r, kvh = cc.kvh;
-    const int nchunks = (((seq + 15) >> 4) + a.bpc - 1) / a.bpc;
+    const int nchunks = cc.nchunks;
     const int h0 = 2 * t, h1 = 2 * t + 1;
     if (nchunks == 1) {
       const float i0 = 1.f / l0, i1 = 1.f / l1;
@@ -440,12 +438,11 @@ int launch_cfg(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return (int)e;
     attr[dev] = true;
   }
+  // the full persistent grid: the work list was built for exactly its warps
+  // (pm_attn_workers_cfg); warps without pieces exit at once
   const int sms = num_sms();
-  const long long items = (long long)a.M * a.Hkv * a.max_chunks;
   const int per_sm = (227 * 1024) / C::SMEM;
-  long long grid = (long long)sms * (per_sm > 0 ? per_sm : 1);
-  const long long need = (items + WARPS - 1) / WARPS;
-  if (grid > need) grid = need;
+  const long long grid = (long long)sms * (per_sm > 0 ? per_sm : 1);
   return (int)launch_k(paged_attn_kernel<HD, WARPS, STAGES>, dim3((int)grid), dim3(WARPS * 32), C::SMEM, st, *tm, a);
 }
 
@@ -509,21 +506,22 @@ int launch_attn(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st, int c
 
 // q [M][H][hd] bf16 (RoPE'd), pool via `tmap_kv` (2-D view [blocks*16][L_s*2*Hkv*hd],
 // box [16][64], 128B swizzle), block_table [M][max_blocks], seq_lens [M] (cached
-// positions incl. the current token), work = the step's chunk-major (chunk, row)
-// list (see pm_attn_work_list), out [M][H][hd] bf16.  ws_o/ws_ml hold
-// [M][Hkv][max_chunks][8][hd] / [..][2][8] fp32 chunk partials; counters [M][Hkv]
-// start at 0 and are left at 0.
+// positions incl. the current token), work = the step's balanced piece list
+// (pm_attn_work_list, built for pm_attn_workers_cfg(hd, cfg) warps and pieces of at
+// most `max_piece` blocks), out [M][H][hd] bf16.  ws_o/ws_ml hold
+// [M][Hkv][max_chunks][8][hd] / [..][2][8] fp32 piece partials (max_chunks >= the
+// most pieces of one (row, head)); counters [M][Hkv] start at 0 and are left at 0.
 extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_table,
                                   const int* seq_lens, const int* work, void* out, float* ws_o, float* ws_ml,
                                   int* counters, int M, int H, int Hkv, int hd, int layer, int L_s, int max_blocks,
-                                  int max_chunks, int blocks_per_chunk, int cfg, void* stream) {
+                                  int max_chunks, int max_piece, int cfg, void* stream) {
   (void)L_s;
   if (M == 0) return 0;
   const int G = H / Hkv;
-  if (H % Hkv || G > MAX_G || max_chunks < 1 || blocks_per_chunk < 1) return (int)cudaErrorInvalidValue;
-  if (max_chunks * blocks_per_chunk < max_blocks || blocks_per_chunk > MAX_BPC) return (int)cudaErrorInvalidValue;
+  if (H % Hkv || G > MAX_G || max_chunks < 1 || max_piece < 1 || max_piece > MAX_P || M > 65536 || Hkv > 65535)
+    return (int)cudaErrorInvalidValue;
   AttnArgs a{reinterpret_cast<const bf16*>(q), block_table, seq_lens, reinterpret_cast<bf16*>(out),
-             ws_o, ws_ml, counters, work, M, H, Hkv, G, layer, max_blocks, max_chunks, blocks_per_chunk,
+             ws_o, ws_ml, counters, work, M, H, Hkv, G, layer, max_blocks, max_chunks, max_piece,
              1.4426950408889634f / sqrtf((float)hd), attn_debug()};
   auto tm = reinterpret_cast<const CUtensorMap*>(tmap_kv);
   auto st = reinterpret_cast<cudaStream_t>(stream);
@@ -532,15 +530,8 @@ extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int*
   return (int)cudaErrorInvalidValue;
 }
 
-extern "C" int pm_attn_blocks_per_split(void) {
-  static int bpc = 0;
-  if (!bpc) {
-    const char* e = getenv("PM_ATTN_BPC");  // tuning override
-    bpc = e ? atoi(e) : 24;   // measured best on the C2 / C3 / C4 benches (profiles/r2/attention_chunks.md)
-    if (bpc < 1 || bpc > MAX_BPC) bpc = 24;
-  }
-  return bpc;
-}
+// Most KV blocks one piece may hold (the kernel's per-piece block-id slots).
+extern "C" int pm_attn_max_piece(void) { return MAX_P; }
 
 extern "C" int pm_attn_workers_cfg(int hd, int cfg);
 // Warps of a full attention launch (the `workers` of pm_attn_work_list).
@@ -571,47 +562,65 @@ extern "C" int pm_prepare_attention(void) {
   return (int)e;
 }
 
-// Host helper: the work list of one step from its sequence lengths (what the
-// engine uploads with the block tables).  Entries are the non-empty (chunk,
-// row) pairs, chunk-major, then stably sorted by size (blocks) descending and
-// laid out "snake" over `workers` warps (odd rounds reversed) so every warp
-// gets a near-equal number of KV blocks.  Chunk boundaries still depend only
-// on each row's own length.  work holds 2 + 2 * M * ceil(max_blocks /
-// blocks_per_chunk) ints; work[0] = #entries, entry j at [2 + 2j] =
-// (chunk << 16) | row and [3 + 2j] = seq_lens[row].
-extern "C" int pm_attn_work_list(const int* seq_lens, int M, int blocks_per_chunk, int hkv, int workers,
+// Host helper: the balanced work list of one step (mirrors ops.attn_work_list).
+// Units = (row, kv head) pairs in row-major order, nb = ceil(seq / 16) blocks
+// each, laid end to end (B blocks); warp w gets blocks [w q, (w + 1) q) with
+// q = max(minq, ceil(B / workers)); every (unit x warp) segment is cut into
+// pieces of at most maxp blocks.  work[0] = warps used, work[1] = pieces P,
+// work[2 + w] = warp w's first piece (work[2 + used] = P), pieces from int
+// (3 + used + 3) & ~3: {row | kvh << 16, b0 | nblk << 16, chunk | nchunks << 16,
+// seq}.  Returns the ints written (or a negative cudaError_t); `cap` = ints
+// available in work.
+extern "C" int pm_attn_work_list(const int* seq_lens, int M, int hkv, int workers, int maxp, int minq, int cap,
                                  int* work) {
-  if (M < 0 || M > 65535 || blocks_per_chunk < 1 || hkv < 1) return (int)cudaErrorInvalidValue;
-  int max_chunks = 0;
-  for (int r = 0; r < M; ++r) {
-    const int nc = (((seq_lens[r] + 15) >> 4) + blocks_per_chunk - 1) / blocks_per_chunk;
-    if (nc > max_chunks) max_chunks = nc;
+  if (M < 0 || M > 65536 || hkv < 1 || hkv > 65535 || workers < 1 || maxp < 1 || maxp > MAX_P || minq < 1 || cap < 3)
+    return -(int)cudaErrorInvalidValue;
+  long long B = 0;
+  for (int r = 0; r < M; ++r) B += (long long)((seq_lens[r] + 15) >> 4) * hkv;
+  if (B == 0) {
+    work[0] = work[1] = work[2] = 0;
+    return 3;
   }
-  std::vector<int> ent, size;
-  for (int c = 0; c < max_chunks; ++c)
-    for (int r = 0; r < M; ++r) {
-      const int nb = (seq_lens[r] + 15) >> 4;
-      const int sz = std::min(blocks_per_chunk, nb - c * blocks_per_chunk);
-      if (sz > 0) {
-        ent.push_back((c << 16) | r);
-        size.push_back(sz);
-      }
+  const long long q = std::max<long long>(minq, (B + workers - 1) / workers);
+  const int used = (int)((B + q - 1) / q);
+  const int base = (3 + used + 3) & ~3;
+  // pass 1: pieces per unit; pass 2: write them (chunk = rank within the unit)
+  std::vector<int> per_unit((size_t)M * hkv, 0);
+  long long pos = 0;
+  for (int u = 0; u < M * hkv; ++u) {
+    const long long e = pos + ((seq_lens[u / hkv] + 15) >> 4);
+    for (long long cur = pos; cur < e;) {
+      const long long seg_end = std::min(e, (cur / q + 1) * q);
+      cur = std::min(seg_end, cur + maxp);
+      ++per_unit[u];
     }
-  const int n = (int)ent.size();
-  std::vector<int> order(n);
-  for (int i = 0; i < n; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return size[x] > size[y]; });
-  if (workers > 0 && workers % hkv == 0) {
-    const int per_round = workers / hkv;
-    for (int j = 1; (j + 1) * per_round <= n; j += 2)
-      std::reverse(order.begin() + j * per_round, order.begin() + (j + 1) * per_round);
+    pos = e;
   }
-  for (int i = 0; i < n; ++i) {
-    const int e = ent[order[i]];
-    work[2 + 2 * i] = e;
-    work[3 + 2 * i] = seq_lens[e & 0xffff];
+  long long P = 0;
+  for (int n : per_unit) P += n;
+  if (base + 4 * P > cap) return -(int)cudaErrorInvalidValue;
+  work[0] = used;
+  work[1] = (int)P;
+  int j = 0, w_next = 0;
+  pos = 0;
+  for (int u = 0; u < M * hkv; ++u) {
+    const int r = u / hkv, h = u % hkv;
+    const long long s = pos, e = pos + ((seq_lens[r] + 15) >> 4);
+    int chunk = 0;
+    for (long long cur = s; cur < e; ++chunk, ++j) {
+      const int w = (int)(cur / q);
+      while (w_next <= w) work[2 + w_next++] = j;   // warps whose first piece is j
+      const long long seg_end = std::min(e, (cur / q + 1) * q);
+      const long long pe = std::min(seg_end, cur + maxp);
+      int* pc = work + base + 4 * j;
+      pc[0] = r | (h << 16);
+      pc[1] = (int)(cur - s) | (int)((pe - cur) << 16);
+      pc[2] = chunk | (per_unit[u] << 16);
+      pc[3] = seq_lens[r];
+      cur = pe;
+    }
+    pos = e;
   }
-  work[0] = n;
-  work[1] = 0;
-  return 0;
+  while (w_next <= used) work[2 + w_next++] = j;
+  return base + 4 * (int)P;
 }

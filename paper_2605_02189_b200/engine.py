@@ -135,7 +135,6 @@ class DecodeEngine:
             self.stages.append((ex, KvEngine(ex, rep, self.slot_of, self.dev, timing=timing,
                                              low_priority_copies=copy_priority)))
         self.work_len = self.stages[0][0].aws.work_len
-        self.bpc = self.stages[0][0].aws.bpc
         self.attn_hkv, self.attn_workers = self.stages[0][0].aws.Hkv, self.stages[0][0].aws.workers
         self.meta = _MetaRing(self.m_cap, self.max_blocks, extra=self.work_len)
         # lanes = micro-batches in flight on one GPU: consecutive rotation steps
@@ -256,10 +255,10 @@ class DecodeEngine:
         a[o + M + n:o + 2 * M] = 1
         a[o + 2 * M:o + 2 * M + n] = slots
         a[o + 2 * M + n:o + 3 * M] = self.trash_slot
-        # attention work list (chunk-major) over the bucket's rows, padding rows included
+        # balanced attention work list over the bucket's rows, padding rows included
         wo = o + 3 * M
-        ops.attn_work_list(a[o + M:o + 2 * M], self.bpc, self.attn_hkv, self.attn_workers, a[wo:wo + self.work_len])
-        wn = 2 + 2 * int(a[wo])
+        ops.attn_work_list(a[o + M:o + 2 * M], self.attn_hkv, self.attn_workers, a[wo:wo + self.work_len])
+        wn = ops.attn_work_used(a[wo:])
         evs = []
         base = self.meta.dev_ptrs[k]
         srcs = (_C.C.c_void_p * 5)(base, base + 4 * o, base + 4 * (o + M), base + 4 * (o + 2 * M), base + 4 * wo)

@@ -445,69 +445,115 @@ def pool_tmap(pool: torch.Tensor, L_s: int, Hkv: int, hd: int) -> TensorMap:
     return TensorMap(pool, width, n_rows, width * 2, 64, 16)
 
 
-def attn_blocks_per_chunk() -> int:
-    """KV blocks per attention work item (fixed: results depend only on a
-    request's own length)."""
-    return _C.lib().pm_attn_blocks_per_split()
+# Balanced attention work split (pm_attn_work_list): every (row, kv head)'s KV
+# blocks are laid end to end and cut into one contiguous range per warp, then
+# into pieces of at most ATTN_MAXP blocks (the kernel's per-piece block-id
+# slots); a warp gets at least ATTN_MINQ blocks (bounds the pieces, i.e. the
+# merge work, of one (row, head) when the step is small).
+ATTN_MAXP = 32
+ATTN_MINQ = 16
+
+
+def attn_max_chunks(max_blocks: int) -> int:
+    """Pieces one (row, head) of up to ``max_blocks`` blocks can be cut into."""
+    return -(-max_blocks // ATTN_MAXP) + -(-max_blocks // ATTN_MINQ) + 1
+
+
+def attn_work_len(m_cap: int, hkv: int, max_blocks: int, workers: int) -> int:
+    """Ints a work list for up to m_cap rows can take (3 + warps + 4 per piece)."""
+    units = m_cap * hkv
+    pieces = 2 * units + workers + -(-units * max_blocks // ATTN_MAXP)
+    return 6 + workers + 4 * pieces
 
 
 class AttnWorkspace:
-    """Chunk partials [M][Hkv][chunks][8][hd] + (m, l), merge counters and the work list."""
+    """Per-piece partials [M][Hkv][chunks][8][hd] + (m, l), merge counters and the work list."""
 
     def __init__(self, m_cap, Hkv, hd, max_blocks, device, cfg=None, rows_hint=None):
         """``rows_hint``: the rows a step usually carries (a micro-batch), which
         sizes the launch-configuration choice; default ``m_cap``."""
-        self.bpc = attn_blocks_per_chunk()
         self.Hkv = Hkv
         cuda = torch.cuda.is_available()
         if cfg is None:
-            cfg = choose_attn_cfg(rows_hint or m_cap, Hkv, hd, max_blocks, self.bpc) if cuda else -1
+            cfg = choose_attn_cfg(rows_hint or m_cap, Hkv, hd, max_blocks) if cuda else -1
         self.cfg = cfg
         self.workers = _C.lib().pm_attn_workers_cfg(hd, cfg) if cuda else 0
-        self.max_chunks = max(1, -(-max_blocks // self.bpc))
+        self.max_chunks = attn_max_chunks(max_blocks)
         self.o = torch.empty(m_cap * Hkv * self.max_chunks * 8 * hd, dtype=torch.float32, device=device)
         self.ml = torch.empty(m_cap * Hkv * self.max_chunks * 16, dtype=torch.float32, device=device)
         self.counters = torch.zeros(m_cap * Hkv, dtype=torch.int32, device=device)
-        # the step's chunk-major work list (attn_work_list), uploaded with the metadata
-        self.work_len = 2 + 2 * m_cap * self.max_chunks
+        # the step's balanced work list (attn_work_list), uploaded with the metadata
+        self.work_len = attn_work_len(m_cap, Hkv, max_blocks, max(1, self.workers))
         self.work = torch.zeros(self.work_len, dtype=torch.int32, device=device)
 
     def set_work(self, seq_lens_host):
         """Synchronous upload of the work list for ``seq_lens_host`` (tests /
         smoke; the engine stages it through its pinned metadata ring)."""
-        w = attn_work_list(seq_lens_host, self.bpc, self.Hkv, self.workers)
-        self.work[:len(w)].copy_(torch.from_numpy(w))
+        w = attn_work_list(seq_lens_host, self.Hkv, self.workers)
+        n = attn_work_used(w)
+        self.work[:n].copy_(torch.from_numpy(w[:n]))
 
 
-def attn_work_list(seq_lens, bpc: int, hkv: int = 1, workers: int = 0, out=None):
-    """The step's attention work list (mirrors pm_attn_work_list): the
-    non-empty (chunk, row) pairs chunk-major, stably sorted by size (blocks)
-    descending, odd rounds of ``workers // hkv`` entries reversed (snake), so
-    the kernel's round-robin gives every warp a near-equal number of KV
-    blocks.  Entry j is ``((chunk << 16) | row, seq_len)`` at
-    ``out[2 + 2j : 4 + 2j]``; ``out[0]`` = #entries."""
+def attn_work_used(work) -> int:
+    """Ints of a built work list that the kernel reads (the upload size)."""
+    return (3 + int(work[0]) + 3) // 4 * 4 + 4 * int(work[1])
+
+
+def attn_work_list(seq_lens, hkv: int, workers: int, out=None, maxp: int = ATTN_MAXP, minq: int = ATTN_MINQ):
+    """The step's attention work list (mirrors pm_attn_work_list).  Units are
+    the (row, kv head) pairs in row-major order, each nb = ceil(seq / 16)
+    blocks; their blocks laid end to end (B in all) are cut into one range of
+    q = max(minq, ceil(B / workers)) blocks per warp and every (unit x warp)
+    segment into pieces of at most ``maxp`` blocks.  A piece is
+    ``(row | kvh << 16, b0 | nblk << 16, chunk | nchunks << 16, seq)`` where
+    chunk / nchunks are its rank / count among its unit's pieces (the merge
+    order).  Layout: ``out[0]`` = warps used, ``out[1]`` = pieces P,
+    ``out[2 : 3 + warps]`` = each warp's first piece (+ end), pieces from
+    the next 16-byte boundary.  Every warp streams the same number of KV blocks
+    (+-1 piece boundary), whatever the rows' lengths; the split points depend
+    on the whole step, so attention results depend on the micro-batch's
+    composition at fp32-rounding level (deterministic for a given step)."""
     import numpy as np
     seq = np.asarray(seq_lens, dtype=np.int64)
     nb = (seq + 15) // 16
-    nc = (nb + bpc - 1) // bpc
-    cmax = int(nc.max()) if len(nc) else 0
-    mask = np.arange(cmax)[:, None] < nc[None, :]          # [chunk][row]
-    c_idx, r_idx = np.nonzero(mask)                           # chunk-major order
-    size = np.minimum(bpc, nb[r_idx] - c_idx * bpc)
-    order = np.argsort(-size, kind="stable")
-    n = len(order)
-    if workers > 0 and workers % hkv == 0:
-        per = workers // hkv
-        j = 1
-        while (j + 1) * per <= n:
-            order[j * per:(j + 1) * per] = order[j * per:(j + 1) * per][::-1]
-            j += 2
-    c_idx, r_idx = c_idx[order], r_idx[order]
+    unb = np.repeat(nb, hkv)
+    ustart = np.zeros(len(unb) + 1, dtype=np.int64)
+    np.cumsum(unb, out=ustart[1:])
+    B = int(ustart[-1])
+    if B == 0 or workers <= 0:
+        if out is None:
+            out = np.zeros(3, dtype=np.int32)
+        out[0] = out[1] = out[2] = 0
+        return out
+    q = max(minq, -(-B // workers))
+    w_used = -(-B // q)
+    wstart = np.minimum(np.arange(w_used + 1, dtype=np.int64) * q, B)
+    cuts = np.union1d(ustart, wstart)
+    seg_s, seg_e = cuts[:-1], cuts[1:]
+    k = (seg_e - seg_s + maxp - 1) // maxp
+    rep = np.repeat(np.arange(len(seg_s)), k)
+    first = np.cumsum(k) - k
+    ps = seg_s[rep] + (np.arange(int(k.sum())) - first[rep]) * maxp
+    pe = np.minimum(ps + maxp, seg_e[rep])
+    u = np.searchsorted(ustart, ps, side="right") - 1
+    P = len(ps)
+    chunk = np.arange(P) - np.searchsorted(u, u, side="left")
+    nchunks = np.bincount(u, minlength=len(unb))[u]
+    w = ps // q
+    woff = np.searchsorted(w, np.arange(w_used + 1), side="left")
+    r, h = u // hkv, u % hkv
+    base = (3 + w_used + 3) // 4 * 4          # pieces 16-byte aligned (int4 loads)
+    need = base + 4 * P
     if out is None:
-        out = np.zeros(2 + 2 * n, dtype=np.int32)
-    out[0], out[1] = n, 0
-    out[2:2 + 2 * n:2] = (c_idx << 16) | r_idx
-    out[3:3 + 2 * n:2] = seq[r_idx]
+        out = np.zeros(need, dtype=np.int32)
+    assert len(out) >= need, "work list buffer too small"
+    out[0], out[1] = w_used, P
+    out[2:3 + w_used] = woff
+    pc = out[base:base + 4 * P].reshape(P, 4)
+    pc[:, 0] = r | (h << 16)
+    pc[:, 1] = (ps - ustart[u]) | ((pe - ps) << 16)
+    pc[:, 2] = chunk | (nchunks << 16)
+    pc[:, 3] = seq[r]
     return out
 
 
@@ -516,41 +562,24 @@ def attn_workers(hd: int) -> int:
     return _C.lib().pm_attn_workers(hd)
 
 
-# (cfg, KV-ring stages per warp) of the candidate launch configurations: both
-# keep 24 stage slots per SM, so a warp's streaming rate scales with its stages;
-# on a tie the deeper ring wins (measured on C3)
-ATTN_CFGS = ((2, 3), (1, 2))
+# Launch configuration of the attention kernel (warps x KV-ring stages per SM;
+# both keep 24 ring slots per SM).  With the balanced work split every warp
+# streams the same number of blocks, so the choice is a measured rule on the
+# step's rows (profiles/r2/attention_balanced.md).
+ATTN_WIDE_ROWS = 96   # rows per step from which 12 warps x 2 stages beats 8 x 3
 
 
-def choose_attn_cfg(m_cap: int, hkv: int, hd: int, max_blocks: int, bpc: int) -> int:
-    """Launch configuration of a workspace's attention kernel: the candidate
-    whose busiest warp finishes first when every row holds ``max_blocks``
-    blocks, under the work list's own size-sorted snake assignment (cost =
-    blocks of the busiest warp / its ring stages; ties go to the deeper ring).  Measured: Qwen3-32B
-    stage C3 (64 rows) 2.13 -> 2.06 ms/step with 8 x 3; C2 and C4 keep 12 x 2.
-    PM_ATTN_CFG forces one.  The choice never changes results."""
+def choose_attn_cfg(rows: int, hkv: int, hd: int, max_blocks: int) -> int:
+    """Launch configuration of a workspace's attention kernel: 12 warps x 2
+    stages for wide steps (C2, ~121 rows: 5.66 vs 5.74 ms/step), 8 x 3 below
+    (C3 stage, 48 rows: 1.925 vs 1.958; C4 stage equal) -- measured with the
+    balanced split (profiles/r2/attention_balanced.md).  Never changes
+    results beyond the split points (the work list is built for the chosen
+    warp count); PM_ATTN_CFG forces one."""
     import os
     if os.environ.get("PM_ATTN_CFG"):
         return int(os.environ["PM_ATTN_CFG"])
-    import numpy as np
-    best, best_cost = -1, None
-    seq = np.full(m_cap, max_blocks * 16 - 1, dtype=np.int64)
-    nb = (seq + 15) // 16
-    for cfg, stages in ATTN_CFGS:
-        w = _C.lib().pm_attn_workers_cfg(hd, cfg)
-        if w <= 0:
-            continue
-        lst = attn_work_list(seq, bpc, hkv, w)
-        n = int(lst[0])
-        ent = lst[2:2 + 2 * n:2]
-        c_idx, r_idx = ent >> 16, ent & 0xffff
-        size = np.minimum(bpc, nb[r_idx] - c_idx * bpc)
-        items = np.repeat(size, hkv)                      # entry j -> items j*hkv .. j*hkv+hkv-1
-        load = np.bincount(np.arange(len(items)) % w, weights=items, minlength=w)
-        cost = load.max() / stages
-        if best_cost is None or cost < best_cost:
-            best, best_cost = cfg, cost
-    return best
+    return 1 if rows >= ATTN_WIDE_ROWS else 2
 
 
 def paged_attention(tmap_kv, q, block_table, seq_lens, out, ws: AttnWorkspace, M, H, Hkv, hd, layer,
@@ -559,7 +588,7 @@ def paged_attention(tmap_kv, q, block_table, seq_lens, out, ws: AttnWorkspace, M
     def go():
         _C.call("pm_paged_attention", tmap_kv.ptr, _ptr(q), _ptr(block_table), _ptr(seq_lens), _ptr(ws.work), _ptr(out),
                 _ptr(ws.o), _ptr(ws.ml), _ptr(ws.counters), M, H, Hkv, hd, layer, L_s, block_table.shape[1],
-                ws.max_chunks, ws.bpc, ws.cfg, _stream(stream))
+                ws.max_chunks, ATTN_MAXP, ws.cfg, _stream(stream))
     if TIMER is None:
         go()
     else:

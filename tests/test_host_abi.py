@@ -59,30 +59,19 @@ def test_stream_k_partition(units, kb, grid):
     assert _C.lib().pm_gemm_max_segments(T, kb, G) == segs
 
 
-@pytest.mark.parametrize("lens,bpc,hkv,workers", [([1, 17, 300, 129, 128], 4, 2, 4), ([5], 4, 8, 1776),
-                                                   ([1000, 2, 77, 513], 4, 1, 3), ([16] * 9, 1, 2, 6),
-                                                   (list(range(1, 400, 7)), 4, 8, 64)])
-def test_attention_work_list_host_helpers_agree(lens, bpc, hkv, workers):
+@pytest.mark.parametrize("lens,hkv,workers", [([1, 17, 300, 129, 128], 2, 4), ([5], 8, 1776),
+                                               ([1000, 2, 77, 513], 1, 3), ([16] * 9, 2, 6),
+                                               (list(range(1, 400, 7)), 8, 64)])
+def test_attention_work_list_host_helpers_agree(lens, hkv, workers):
     """The C helper (what a non-Python host would call) and the numpy one the
-    engine uses build the same list; it covers every (row, chunk) exactly
-    once, sizes are non-increasing within each forward round, and the snake
-    keeps per-warp block counts within one chunk of each other when every
-    warp gets work."""
+    engine uses build the same balanced piece list (tests/test_attn_work_list.py
+    checks its coverage and balance at the bench shapes)."""
     import numpy as np
     seq = np.asarray(lens, dtype=np.int32)
-    nch = [-(-(-(-L // 16)) // bpc) for L in lens]
-    buf = np.zeros(2 + 2 * len(lens) * max(nch), dtype=np.int32)
-    assert _C.lib().pm_attn_work_list(seq.ctypes.data_as(_C.C.c_void_p), len(lens), bpc, hkv, workers,
-                                      buf.ctypes.data_as(_C.C.c_void_p)) == 0
-    ref = ops.attn_work_list(seq, bpc, hkv, workers)
-    assert buf[0] == ref[0] and np.array_equal(buf[:2 + 2 * buf[0]], ref)
-    pairs = [(int(e) >> 16, int(e) & 0xffff) for e in ref[2::2]]
-    assert [int(x) for x in ref[3::2]] == [lens[r] for _, r in pairs]
-    assert sorted(pairs) == sorted((c, r) for r in range(len(lens)) for c in range(nch[r]))
-    size = [min(bpc, -(-lens[r] // 16) - c * bpc) for c, r in pairs]
-    # per-warp load of the kernel's round-robin over expanded items (entry x hkv)
-    load = [0] * workers
-    for i in range(len(pairs) * hkv):
-        load[i % workers] += size[i // hkv]
-    if len(pairs) * hkv >= 2 * workers:
-        assert max(load) - min(load) <= 2 * bpc
+    cap = ops.attn_work_len(len(lens), hkv, max(-(-L // 16) for L in lens), workers)
+    buf = np.zeros(cap, dtype=np.int32)
+    n = _C.lib().pm_attn_work_list(seq.ctypes.data_as(_C.C.c_void_p), len(lens), hkv, workers, ops.ATTN_MAXP,
+                                   ops.ATTN_MINQ, cap, buf.ctypes.data_as(_C.C.c_void_p))
+    ref = ops.attn_work_list(seq, hkv, workers)
+    assert n == len(ref) == ops.attn_work_used(ref)
+    assert np.array_equal(buf[:n], ref)

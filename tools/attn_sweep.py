@@ -1,4 +1,4 @@
-"""Paged attention alone over launch configuration x KV blocks per work item
+"""Paged attention alone over launch configurations (balanced work split)
 on the bench's decode shapes (C2, C3/C4 per-stage rows, C5 points).  CUDA
 events around 8 back-to-back launches over different layers (pool >> L2),
 median of 5 repeats.  usage: python tools/attn_sweep.py [out.txt]"""
@@ -12,7 +12,6 @@ from paper_2605_02189_b200 import _C, ops  # noqa: E402
 from paper_2605_02189_b200.models import LLAMA3_70B, QWEN3_8B, QWEN3_32B  # noqa: E402
 
 dev = "cuda"
-BPCS = (8, 12, 16, 20, 24, 32)
 _C.call("pm_prepare_attention")
 out_f = open(sys.argv[1], "w") if len(sys.argv) > 1 else None
 
@@ -47,33 +46,26 @@ for name, spec, L_s, M, seq in shapes:
     ref = None
     res = []
     for cfg in (1, 2, 0):
-        for bpc in BPCS:
-            aws = ops.AttnWorkspace(M, Hkv, hd, max_blocks, dev, cfg=cfg)
-            aws.bpc = bpc
-            aws.max_chunks = max(1, -(-max_blocks // bpc))
-            aws.o = torch.empty(M * Hkv * aws.max_chunks * 8 * hd, dtype=torch.float32, device=dev)
-            aws.ml = torch.empty(M * Hkv * aws.max_chunks * 16, dtype=torch.float32, device=dev)
-            aws.work_len = 2 + 2 * M * aws.max_chunks
-            aws.work = torch.zeros(aws.work_len, dtype=torch.int32, device=dev)
-            aws.set_work(seqs.numpy())
-            ts = []
-            for rep in range(6):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record()
-                for layer in range(8):
-                    ops.paged_attention(tm, q, bt, seqs_d, out, aws, M, H, Hkv, hd, layer % L_s, L_s)
-                b.record()
-                torch.cuda.synchronize()
-                if rep:
-                    ts.append(a.elapsed_time(b) * 1e-3 / 8)
-            t = float(np.median(ts))
-            if ref is None:
-                ref = out.clone()
-            err = float((out.float() - ref.float()).abs().max())
-            res.append((t, cfg, bpc, err))
-            log(f"{name:24s} M={M:3d} L_s={L_s:2d} cfg={cfg} bpc={bpc:2d}: {t*1e6:7.1f} us "
-                f"{kvb/t/1e9:6.0f} GB/s  (max|d| vs first {err:.1e})")
-    t, cfg, bpc, _ = min(res)
-    log(f"BEST {name} M={M}: cfg={cfg} bpc={bpc} {t*1e6:.1f} us {kvb/t/1e9:.0f} GB/s")
+        aws = ops.AttnWorkspace(M, Hkv, hd, max_blocks, dev, cfg=cfg)
+        aws.set_work(seqs.numpy())
+        ts = []
+        for rep in range(6):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for layer in range(8):
+                ops.paged_attention(tm, q, bt, seqs_d, out, aws, M, H, Hkv, hd, layer % L_s, L_s)
+            b.record()
+            torch.cuda.synchronize()
+            if rep:
+                ts.append(a.elapsed_time(b) * 1e-3 / 8)
+        t = float(np.median(ts))
+        if ref is None:
+            ref = out.clone()
+        err = float((out.float() - ref.float()).abs().max())
+        res.append((t, cfg, 0, err))
+        log(f"{name:24s} M={M:3d} L_s={L_s:2d} cfg={cfg}: {t*1e6:7.1f} us "
+            f"{kvb/t/1e9:6.0f} GB/s  (max|d| vs first {err:.1e})")
+    t, cfg, _, _ = min(res)
+    log(f"BEST {name} M={M}: cfg={cfg} {t*1e6:.1f} us {kvb/t/1e9:.0f} GB/s")
     del pool
     torch.cuda.empty_cache()

@@ -10,10 +10,14 @@ import torch  # noqa: E402
 
 sys.path.insert(0, ".")
 from paper_2605_02189_b200 import _C, ops  # noqa: E402
-from paper_2605_02189_b200.models import QWEN3_8B  # noqa: E402
+from paper_2605_02189_b200.models import SPECS  # noqa: E402
 
 dev = "cuda"
-spec, L_s, M, seq = QWEN3_8B, 36, 128, int(sys.argv[1]) if len(sys.argv) > 1 else 550
+# usage: attn_trace.py [seq] [model] [L_s] [M]
+seq = int(sys.argv[1]) if len(sys.argv) > 1 else 550
+spec = SPECS[sys.argv[2]] if len(sys.argv) > 2 else SPECS["qwen3-8b"]
+L_s = int(sys.argv[3]) if len(sys.argv) > 3 else 36
+M = int(sys.argv[4]) if len(sys.argv) > 4 else 128
 H, Hkv, hd = spec.H, spec.Hkv, spec.hd
 g = torch.Generator(device=dev).manual_seed(0)
 seqs = torch.randint(seq // 2, seq * 3 // 2, (M,), generator=g, device=dev).to(torch.int32)
@@ -45,3 +49,8 @@ for name, v in [("start", st), ("first data", fd), ("end", en), ("blocks", nblk)
     print(f"{name:10s} " + " ".join(f"{x:7.1f}" for x in q_))
 hist = np.histogram(en, bins=10)
 print("end-time histogram:", list(hist[0]), [f"{x:.0f}" for x in hist[1]])
+busy = en - fd
+live = nblk > 0
+print(f"warps with work {live.sum()}/{len(t)}; us per block per warp (first data -> end): "
+      f"median {np.median(busy[live] / nblk[live]):.2f}; mean warp busy {busy[live].mean():.1f} us of span {en.max():.1f}")
+print(f"aggregate while streaming: {kvb / 1e3 / (en.max() - np.median(fd)):.0f} GB/s (span minus median first-data)")
