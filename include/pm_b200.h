@@ -75,19 +75,23 @@ int pm_rmsnorm(const float* x, const void* w, void* y, int M, int d, float eps, 
 int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok, int bn,
             int grid, int cta_pair, int epilogue, void* out, int ld_out, float* ws, int max_segs, float* amax_val,
             int* amax_idx, int m_cap, const void* prefetch, unsigned long long prefetch_bytes,
-            unsigned long long prefetch_span, int* fix_counters, const int* fix_units, int n_fix, void* stream);
+            unsigned long long prefetch_span, int fix_mode, int* fix_counters, const int* fix_units, int n_fix,
+            void* stream);
 /* prefetch/prefetch_bytes: optional region the NEXT operation reads first; it is pulled into L2 while
  * this GEMM drains (keeps HBM busy across the kernel boundary); NULL/0 for none.  prefetch_span = 0:
  * the contiguous [prefetch, +prefetch_bytes); > 0: one stripe of prefetch_bytes / grid per CTA, stripe c
  * at prefetch + c * prefetch_span / grid -- the first bytes of every stream-K worker's range when the
  * next operation is a GEMM over prefetch_span bytes of packed weight (its workers start at evenly spaced
  * k-blocks). */
-/* fix_counters = NULL: split units are finished by a post kernel (launched on `stream` after the GEMM).
- * fix_counters = int[2 * n_units] (zero at rest, left zero): the GEMM kernel finishes them itself --
- * fixup tasks over the n_fix units in fix_units (the split units, pm_gemm_fix_units; every unit for
- * pm_gemm_qkv_rope), equal shares per CTA, each waiting on its unit's segment arrivals.  Needs every
- * CTA of the grid resident at once (one stream of dependent kernels, not two concurrent lanes) and
- * m_tok <= bn. */
+/* fix_mode: how the units the stream-K partition splits are finished.
+ *   0: a post kernel on `stream` waits for the whole GEMM grid, then finishes them;
+ *   2 (poll): the GEMM arrives on fix_counters[unit] as each part lands and every post-kernel CTA starts
+ *      as soon as its own unit is complete (overlapping the GEMM's tail); the post kernel still completes
+ *      only after the GEMM grid.  Deadlock-free (the post kernel launches after every GEMM CTA started);
+ *   1 (fused): the GEMM kernel itself runs fixup tasks over the n_fix units in fix_units (the split
+ *      units, pm_gemm_fix_units; every unit for pm_gemm_qkv_rope), each waiting on its unit's arrivals --
+ *      needs every CTA of the grid resident at once (one stream of dependent kernels) and m_tok <= bn.
+ * fix_counters: int[2 * n_units], zero at rest, left zero (modes 1 and 2). */
 /* residual projection (O / down) fused with the next RMSNorm: resid += X W^T (fp32), then
  * xn = RMSNorm(resid) * norm_w (bf16) per row; row_counters int[m_cap], zero at rest, left zero.
  * split_norm = 0: the last unit to finish a row normalises it inside the fixup kernel;
@@ -95,14 +99,14 @@ int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, in
 int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
                           int bn, int grid, int cta_pair, float* resid, float* ws, int max_segs, int m_cap, const void* prefetch,
                           unsigned long long prefetch_bytes, unsigned long long prefetch_span, const void* norm_w, void* xn, float eps,
-                          int* row_counters, int split_norm, int* fix_counters, const int* fix_units, int n_fix,
-                          void* stream);
+                          int* row_counters, int split_norm, int fix_mode, int* fix_counters, const int* fix_units,
+                          int n_fix, void* stream);
 /* QKV projection fused with (Qwen3 q/k RMSNorm) + RoPE + paged KV append (pm_qkv_rope_append's contract);
  * qkv_out [m_cap][n_out] bf16 is scratch */
 int pm_gemm_qkv_rope(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok, int bn,
                      int grid, int cta_pair, void* qkv_out, float* ws, int max_segs, int m_cap, const void* prefetch,
-                     unsigned long long prefetch_bytes, unsigned long long prefetch_span, int* fix_counters,
-                     const int* fix_units, int n_fix, void* q_out, void* pool, const int* block_table,
+                     unsigned long long prefetch_bytes, unsigned long long prefetch_span, int fix_mode,
+                     int* fix_counters, const int* fix_units, int n_fix, void* q_out, void* pool, const int* block_table,
                      const int* positions, const float* rope, const void* qn_w, const void* kn_w, int H, int Hkv,
                      int hd, int layer, int L_s, int max_blocks, float eps, void* stream);
 /* stream-K geometry helpers over `workers` (= grid, or grid / 2 in pair mode) */

@@ -30,9 +30,9 @@ _SIGS = {
     "pm_copy_pieces": [_P, _P, _P, _P, _I, _U64, _P],
     "pm_offload_gather": [_P, _P, _P, _P, _I, _U64, _P, _P, _P],
     "pm_copy_2d": [_P, _U64, _P, _U64, _U64, _U64, _P],
-    "pm_gemm": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _P, _I, _P, _U64, _U64, _P, _P, _I, _P],
-    "pm_gemm_resid_rmsnorm": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _I, _I, _P, _U64, _U64, _P, _P, _F, _P, _I, _P, _P, _I, _P],
-    "pm_gemm_qkv_rope": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _I, _I, _P, _U64, _U64, _P, _P, _I, _P, _P, _P, _P, _P, _P,
+    "pm_gemm": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _P, _I, _P, _U64, _U64, _I, _P, _P, _I, _P],
+    "pm_gemm_resid_rmsnorm": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _I, _I, _P, _U64, _U64, _P, _P, _F, _P, _I, _I, _P, _P, _I, _P],
+    "pm_gemm_qkv_rope": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _I, _I, _P, _U64, _U64, _I, _P, _P, _I, _P, _P, _P, _P, _P, _P,
                          _P, _I, _I, _I, _I, _I, _I, _F, _P],
     "pm_gemm_split_units": [_LL, _I, _I],
     "pm_gemm_split_event": [_P],

@@ -68,14 +68,24 @@ struct GemmArgs {
   long long total;    // units * tok_tiles * kb
   int debug;          // profiling only: bit0 skip epilogue math, bit2 skip partial stores, bit3 trace,
                       // bit4 skip the fixup/post kernel (bits 5/6/7: only reduce / resid-norm / qkv-rope)
-  int fused;          // 1: split units are finished inside this kernel (fused_fixup), no post kernel
+  int fix_mode;       // FixMode: how split units are finished
   int post;           // Post: what the fixup applies (plain epilogue / residual + RMSNorm / q-k norm + RoPE)
-  int* unit_cnt;      // fused: [units] segment arrivals, then [units] finished fixup tasks (zero at rest)
+  int* unit_cnt;      // FIX_FUSED / FIX_POLL: [units] segment arrivals, then [units] readers / finished tasks (zero at rest)
+  int ctas_per_worker;   // 2 in pair mode (both halves arrive), else 1
   const int* fix_units;   // fused: the units with fixup tasks (split units; every unit for the QKV post)
   int n_fix;
 };
 
 enum Post : int { POST_NONE = 0, POST_RESID_NORM = 1, POST_QKV_ROPE = 2 };
+// FIX_POST: the post kernel waits for the whole GEMM grid (griddepcontrol.wait),
+// then finishes the split units.  FIX_POLL: the GEMM arrives per unit as its
+// partials land (release) and each post-kernel CTA starts as soon as ITS unit
+// is complete (acquire), overlapping the GEMM's tail; it still waits for the
+// GEMM grid before it exits, so its completion implies the GEMM's (the next
+// kernel's griddepcontrol.wait keeps its meaning).  Deadlock-free: the post
+// kernel launches only after every GEMM CTA started, and GEMM CTAs never
+// wait on it.  FIX_FUSED: the GEMM kernel finishes the units itself.
+enum FixMode : int { FIX_POST = 0, FIX_FUSED = 1, FIX_POLL = 2 };
 
 struct NormArgs {
   const bf16* w;      // [d] RMSNorm weight
@@ -465,7 +475,7 @@ PM_DEV void fused_fixup(const GemmArgs& a, const NormArgs& na, const RopeArgs& r
             if (s0 + s < nseg && c < a.m_tok)
               asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
                            : "=f"(y[s][j].x), "=f"(y[s][j].y), "=f"(y[s][j].z), "=f"(y[s][j].w)
-                           : "l"(part + ((size_t)(s0 + s) * BN + c) * UNIT_ROWS));
+                           : "l"(part + ((size_t)(s0 + s) * BN + c) * UNIT_ROWS) : "memory");
           }
 #pragma unroll
         for (int j = 0; j < FIX_COLS / 2; ++j)
@@ -791,13 +801,13 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a, NormA
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
-      if (FUSED && !(a.debug & 1)) {
+      if ((FUSED || a.fix_mode == FIX_POLL) && !(a.debug & 1)) {
         const int tid = threadIdx.x - EPI_WARP0 * 32;
         if (!whole || a.post == POST_QKV_ROPE) {
           // this CTA's part of the unit is stored (partial, or the whole unit's bf16 for the QKV post)
           epi_bar();
           if (tid == 0) red_release_add(a.unit_cnt + sg.unit, 1);
-        } else if (a.post == POST_RESID_NORM) {
+        } else if (FUSED && a.post == POST_RESID_NORM) {
           resid_arrive(a, na, tok_base, 0, tok_end, NH, red_idx, red_val, tid);
         }
       }
@@ -835,6 +845,23 @@ gemm_stream_kernel(const __grid_constant__ CUtensorMap tmap_x, GemmArgs a, NormA
 }
 
 // ---------------------------------------------------------------- post kernels
+// FIX_POLL: block until every CTA of `unit`'s segments stored its part, then
+// count this CTA as a reader; the last of the `readers` CTAs re-arms both counts.
+PM_DEV void poll_unit(const GemmArgs& a, int unit, int nseg, int readers) {
+  if (threadIdx.x == 0) {
+    const int want = nseg * a.ctas_per_worker;
+    int spins = 0;
+    while (ld_acquire(a.unit_cnt + unit) < want)
+      if (++spins > 8) __nanosleep(32);
+    const int units = a.n_units * a.tok_tiles;
+    if (atom_add_acq_rel(a.unit_cnt + units + unit, 1) + 1 == readers) {
+      a.unit_cnt[unit] = 0;
+      a.unit_cnt[units + unit] = 0;
+    }
+  }
+  __syncthreads();
+}
+
 // One CTA per (unit, RC token columns), thread = row of the 256-row unit.
 // RC is chosen per launch so the grid fits in about one wave (launch()).
 // segment count of stream-K unit `unit` (mirrors get_seg / pm_gemm_max_segments)
@@ -863,7 +890,7 @@ PM_DEV void sum_partials(const GemmArgs& a, int unit, int nseg, int c0, int r, f
       for (int j = 0; j < RC; ++j) {
         float x = 0.f;
         if (s0 + s < nseg)
-          asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(x) : "l"(part + ((size_t)(s0 + s) * BN + j) * UNIT_ROWS));
+          asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(x) : "l"(part + ((size_t)(s0 + s) * BN + j) * UNIT_ROWS) : "memory");
         t[s][j] = x;
       }
 #pragma unroll
@@ -924,12 +951,11 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(GemmArgs a, int grid) 
 // the 256-row unit, so one CTA finishes 4 x RC columns.  Same summation order
 // as sum_partials (bit-identical).  Needs n_out % 4 == 0 and ld_out % 4 == 0.
 template <int BN, int RC>
-__global__ void __launch_bounds__(256) gemm_reduce_v4_kernel(GemmArgs a, int grid) {
-  pdl_trigger();
-  pdl_wait();
+PM_DEV void reduce_v4_body(const GemmArgs& a, int grid) {
   const int unit = blockIdx.x;
   const int nseg = unit_segments(a, unit, grid);
   if (nseg == 1) return;
+  if (a.fix_mode == FIX_POLL) poll_unit(a, unit, nseg, gridDim.y);
   const int tok_tile = unit / a.n_units, wunit = unit % a.n_units;
   const int tok_base = tok_tile * BN;
   const int tok_end = min(BN, a.m_tok - tok_base);
@@ -952,7 +978,7 @@ __global__ void __launch_bounds__(256) gemm_reduce_v4_kernel(GemmArgs a, int gri
         if (s0 + s < nseg)
           asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
                        : "=f"(y.x), "=f"(y.y), "=f"(y.z), "=f"(y.w)
-                       : "l"(part + ((size_t)(s0 + s) * BN + j) * UNIT_ROWS));
+                       : "l"(part + ((size_t)(s0 + s) * BN + j) * UNIT_ROWS) : "memory");
         x[s][j] = y;
       }
 #pragma unroll
@@ -1032,6 +1058,14 @@ __global__ void __launch_bounds__(256) gemm_reduce_v4_kernel(GemmArgs a, int gri
       }
     }
   }
+}
+
+template <int BN, int RC>
+__global__ void __launch_bounds__(256) gemm_reduce_v4_kernel(GemmArgs a, int grid) {
+  pdl_trigger();
+  if (a.fix_mode != FIX_POLL) pdl_wait();
+  reduce_v4_body<BN, RC>(a, grid);
+  if (a.fix_mode == FIX_POLL) pdl_wait();   // complete only after the GEMM grid
 }
 
 // ---------------------------------------------------------------- fused post kernels
@@ -1155,12 +1189,11 @@ __global__ void __launch_bounds__(256, 4) gemm_resid_norm_kernel(GemmArgs a, int
 // Vectorised variant: thread = 4 consecutive rows x 1 token column (16-byte
 // partial and residual accesses); a CTA finishes 4 columns, like RC = 4.
 template <int BN, int V4>
-__global__ void __launch_bounds__(256, 4) gemm_resid_norm_v4_kernel(GemmArgs a, int grid, NormArgs na) {
-  pdl_trigger();
-  pdl_wait();
+PM_DEV void resid_norm_v4_body(const GemmArgs& a, int grid, const NormArgs& na) {
   const int unit = blockIdx.x;
   const int nseg = unit_segments(a, unit, grid);
   if (nseg == 1) return;  // whole units were added by the GEMM epilogue and do not count
+  if (a.fix_mode == FIX_POLL) poll_unit(a, unit, nseg, gridDim.y);
   const int tok_tile = unit / a.n_units, wunit = unit % a.n_units;
   const int tok_base = tok_tile * BN;
   const int tok_end = min(BN, a.m_tok - tok_base);
@@ -1186,7 +1219,7 @@ __global__ void __launch_bounds__(256, 4) gemm_resid_norm_v4_kernel(GemmArgs a, 
         if (s0 + s < nseg)
           asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
                        : "=f"(y[s].x), "=f"(y[s].y), "=f"(y[s].z), "=f"(y[s].w)
-                       : "l"(part + (size_t)(s0 + s) * BN * UNIT_ROWS));
+                       : "l"(part + (size_t)(s0 + s) * BN * UNIT_ROWS) : "memory");
       }
 #pragma unroll
       for (int s = 0; s < 12; ++s) { v.x += y[s].x; v.y += y[s].y; v.z += y[s].z; v.w += y[s].w; }
@@ -1211,7 +1244,16 @@ __global__ void __launch_bounds__(256, 4) gemm_resid_norm_v4_kernel(GemmArgs a, 
     }
   }
   __syncthreads();
+  // the row's whole units come from the GEMM epilogue: with polling, wait for the GEMM grid first
+  if (n_last && a.fix_mode == FIX_POLL) pdl_wait();
   if (n_last) block_rmsnorm_rows<V4>(o, a.ld_out, last_rows, n_last, na.w, na.xn, a.n_out, na.eps);
+}
+template <int BN, int V4>
+__global__ void __launch_bounds__(256, 4) gemm_resid_norm_v4_kernel(GemmArgs a, int grid, NormArgs na) {
+  pdl_trigger();
+  if (a.fix_mode != FIX_POLL) pdl_wait();
+  resid_norm_v4_body<BN, V4>(a, grid, na);
+  if (a.fix_mode == FIX_POLL) pdl_wait();   // complete only after the GEMM grid
 }
 
 // (2) fused QKV projection -> (Qwen3 q/k RMSNorm) + RoPE + paged KV append.
@@ -1318,16 +1360,17 @@ __global__ void __launch_bounds__(256) gemm_qkv_rope_kernel(GemmArgs a, int grid
 // column; 64 threads span the 256-row unit, a CTA finishes 4 columns.  The
 // head's norm and the RoPE partner are shuffles within its HL = hd / 4 lanes.
 template <int BN, int HD>
-__global__ void __launch_bounds__(256) gemm_qkv_rope_v4_kernel(GemmArgs a, int grid, RopeArgs ra) {
+PM_DEV void qkv_rope_v4_body(const GemmArgs& a, int grid, const RopeArgs& ra) {
   constexpr int HL = HD / 4;                       // lanes per head (32 or 16)
-  pdl_trigger();
   const int unit = blockIdx.x;
   const int tok_tile = unit / a.n_units, wunit = unit % a.n_units;
   const int tok_base = tok_tile * BN;
   const int tok_end = min(BN, a.m_tok - tok_base);
+  const int nseg = unit_segments(a, unit, grid);
+  // every unit arrives (whole ones after storing their bf16): wait for this one only
+  if (a.fix_mode == FIX_POLL) poll_unit(a, unit, nseg, gridDim.y);
   const int c = blockIdx.y * 4 + (threadIdx.x >> 6);   // warp-uniform column
   if (c >= tok_end) return;
-  const int nseg = unit_segments(a, unit, grid);
   const int t = threadIdx.x & 63, lane = threadIdx.x & 31;
   const int r = 4 * t, n = wunit * UNIT_ROWS + r;
   const bool row_ok = n < a.n_out;                 // n_out % hd == 0: a head is all in or all out
@@ -1349,7 +1392,7 @@ __global__ void __launch_bounds__(256) gemm_qkv_rope_v4_kernel(GemmArgs a, int g
     const uint2 ww = *reinterpret_cast<const uint2*>(nw + d);
     w4[0] = bf16_lo(ww.x); w4[1] = bf16_hi(ww.x); w4[2] = bf16_lo(ww.y); w4[3] = bf16_hi(ww.y);
   }
-  pdl_wait();
+  if (a.fix_mode != FIX_POLL) pdl_wait();
   float x[4];
   if (nseg > 1) {
     const float* part = a.ws + (size_t)unit * a.max_segs * BN * UNIT_ROWS + (size_t)c * UNIT_ROWS + r;
@@ -1362,7 +1405,7 @@ __global__ void __launch_bounds__(256) gemm_qkv_rope_v4_kernel(GemmArgs a, int g
         if (s0 + s < nseg)
           asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
                        : "=f"(y[s].x), "=f"(y[s].y), "=f"(y[s].z), "=f"(y[s].w)
-                       : "l"(part + (size_t)(s0 + s) * BN * UNIT_ROWS));
+                       : "l"(part + (size_t)(s0 + s) * BN * UNIT_ROWS) : "memory");
       }
 #pragma unroll
       for (int s = 0; s < 12; ++s) { v.x += y[s].x; v.y += y[s].y; v.z += y[s].z; v.w += y[s].w; }
@@ -1374,7 +1417,7 @@ __global__ void __launch_bounds__(256) gemm_qkv_rope_v4_kernel(GemmArgs a, int g
     x[3] = __bfloat162float(__float2bfloat16(v.w));
   } else {
     uint2 q = make_uint2(0u, 0u);
-    if (row_ok) q = *reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(a.out) + (size_t)m * a.ld_out + n);
+    if (row_ok) q = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(a.out) + (size_t)m * a.ld_out + n));
     x[0] = bf16_lo(q.x); x[1] = bf16_hi(q.x); x[2] = bf16_lo(q.y); x[3] = bf16_hi(q.y);
   }
   // shuffles run on every lane (a warp may hold heads of different kinds when hd = 64)
@@ -1415,6 +1458,13 @@ __global__ void __launch_bounds__(256) gemm_qkv_rope_v4_kernel(GemmArgs a, int g
   *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]));
 }
 
+template <int BN, int HD>
+__global__ void __launch_bounds__(256) gemm_qkv_rope_v4_kernel(GemmArgs a, int grid, RopeArgs ra) {
+  pdl_trigger();
+  qkv_rope_v4_body<BN, HD>(a, grid, ra);
+  if (a.fix_mode == FIX_POLL) pdl_wait();   // complete only after the GEMM grid
+}
+
 bool getenv_flag(const char* name) {
   const char* v = getenv(name);
   return v && atoi(v);
@@ -1444,7 +1494,7 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int pos
   cudaError_t e;
   const NormArgs nav = na ? *na : NormArgs{};
   const RopeArgs rav = ra ? *ra : RopeArgs{};
-  auto kern = a.fused ? gemm_stream_kernel<BN, NH, true> : gemm_stream_kernel<BN, NH, false>;
+  auto kern = a.fix_mode == FIX_FUSED ? gemm_stream_kernel<BN, NH, true> : gemm_stream_kernel<BN, NH, false>;
   if (NH == 1)   // grid = 2 x workers: each stream-K worker is a (2,1,1) cluster
     e = launch_k_cluster(kern, dim3(grid), dim3(NUM_THREADS), C::SMEM, st, 2, *tx, a, nav, rav);
   else
@@ -1454,7 +1504,7 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int pos
     cudaEventRecord(g_split_event, st);
     g_split_event = nullptr;
   }
-  if (a.fused) return 0;   // the kernel finished every unit itself
+  if (a.fix_mode == FIX_FUSED) return 0;   // the kernel finished every unit itself
   const int G = NH == 1 ? grid / 2 : grid;
   if ((a.debug & 16) || ((a.debug & 32) && post == POST_NONE) || ((a.debug & 64) && post == POST_RESID_NORM) ||
       ((a.debug & 128) && post == POST_QKV_ROPE))
@@ -1469,13 +1519,15 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int pos
   auto go = [&](auto rcc) -> int {
     constexpr int R = decltype(rcc)::value;
     const dim3 pg((unsigned)units, BN / R);
-    static const bool scalar = getenv_flag("PM_POST_SCALAR");   // A/B: thread-per-row kernels
+    static const bool scalar_env = getenv_flag("PM_POST_SCALAR");   // A/B: thread-per-row kernels
+    const bool scalar = scalar_env && a.fix_mode != FIX_POLL;         // polling exists in the v4 kernels only
     if (post == POST_QKV_ROPE) {   // every unit (whole ones read the stored bf16)
       if (!scalar && BN >= 4) {
         const dim3 g4((unsigned)units, BN / 4);
         if (ra->hd == 128) return (int)launch_k(gemm_qkv_rope_v4_kernel<BN, 128>, g4, dim3(256), 0, st, a, G, *ra);
         if (ra->hd == 64) return (int)launch_k(gemm_qkv_rope_v4_kernel<BN, 64>, g4, dim3(256), 0, st, a, G, *ra);
       }
+      if (a.fix_mode == FIX_POLL) return (int)cudaErrorInvalidValue;
       return (int)launch_k(gemm_qkv_rope_kernel<BN, R>, pg, dim3(256), 0, st, a, G, *ra);
     }
     if (post == POST_RESID_NORM && !scalar && BN >= 4) {
@@ -1491,6 +1543,7 @@ int launch(const CUtensorMap* tx, GemmArgs a, int grid, cudaStream_t st, int pos
     }
     if (BN >= 4 * R && a.n_out % 4 == 0 && a.ld_out % 4 == 0 && !scalar)
       return (int)launch_k(gemm_reduce_v4_kernel<BN, R>, dim3((unsigned)units, BN / (4 * R)), dim3(256), 0, st, a, G);
+    if (a.fix_mode == FIX_POLL) return (int)cudaErrorInvalidValue;
     return (int)launch_k(gemm_reduce_kernel<BN, R>, pg, dim3(256), 0, st, a, G);
   };
   if (rc == 2) return go(std::integral_constant<int, 2>{});
@@ -1594,20 +1647,24 @@ extern "C" int pm_gemm_fix_units(long long total, int kb, int grid, int* out) {
 static int make_args(GemmArgs& a, int& grid, int pair, const void* w_packed, int n_out, int n_units, int k,
                      int m_tok, int bn, int epilogue, void* out, int ld_out, float* ws, int max_segs,
                      float* amax_val, int* amax_idx, int m_cap, const void* prefetch,
-                     unsigned long long prefetch_bytes, unsigned long long prefetch_span, int* fix_counters,
-                     const int* fix_units, int n_fix) {
+                     unsigned long long prefetch_bytes, unsigned long long prefetch_span, int fix_mode,
+                     int* fix_counters, const int* fix_units, int n_fix) {
   if (k % BK || m_tok < 1 || m_tok > m_cap || grid < (pair ? 2 : 1)) return (int)cudaErrorInvalidValue;
   const int tok_tiles = (m_tok + bn - 1) / bn;
   a = GemmArgs{reinterpret_cast<const uint8_t*>(w_packed), n_out, n_units, k / BK, m_tok, tok_tiles, epilogue,
                out, ld_out, ws, max_segs, amax_val, amax_idx, m_cap,
                reinterpret_cast<const uint8_t*>(prefetch), prefetch ? prefetch_bytes : 0ull,
                prefetch ? prefetch_span : 0ull, 0u, (long long)n_units * tok_tiles * (k / BK), 0,
-               fix_counters ? 1 : 0, POST_NONE, fix_counters, fix_units, n_fix};
-  // fused fixup: one token tile, 16-byte row quads (the v4 epilogues' layout), a task list
-  if (fix_counters && (tok_tiles != 1 || n_out % 4 || ld_out % 4 || n_fix < 0 || (n_fix && !fix_units)))
+               fix_mode, POST_NONE, fix_counters, pair ? 2 : 1, fix_units, n_fix};
+  // FIX_FUSED / FIX_POLL: per-unit counters, 16-byte row quads (the v4 epilogues' layout);
+  // FIX_FUSED also one token tile and a task list
+  if (fix_mode < FIX_POST || fix_mode > FIX_POLL || (fix_mode != FIX_POST && !fix_counters) ||
+      (fix_mode != FIX_POST && (n_out % 4 || ld_out % 4)) ||
+      (fix_mode == FIX_FUSED && (tok_tiles != 1 || n_fix < 0 || (n_fix && !fix_units))))
     return (int)cudaErrorInvalidValue;
   const Knobs& kn = knobs();
   a.debug = kn.debug;
+  if (a.fix_mode == FIX_POLL && (a.debug & (1 | 16 | 32 | 64 | 128))) a.fix_mode = FIX_POST;   // profiling modes
   a.pf_ahead = kn.pf_ahead;
   if (kn.grid > 0) grid = kn.grid;   // tuning experiments only
   // grid = CTAs; a worker is one CTA, or a 2-CTA cluster in pair mode; at
@@ -1635,12 +1692,12 @@ static int dispatch_bn(int bn, F&& f) {
 extern "C" int pm_gemm(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
                        int bn, int grid, int cta_pair, int epilogue, void* out, int ld_out, float* ws, int max_segs,
                        float* amax_val, int* amax_idx, int m_cap, const void* prefetch,
-                       unsigned long long prefetch_bytes, unsigned long long prefetch_span, int* fix_counters,
-                       const int* fix_units, int n_fix, void* stream) {
+                       unsigned long long prefetch_bytes, unsigned long long prefetch_span, int fix_mode,
+                       int* fix_counters, const int* fix_units, int n_fix, void* stream) {
   GemmArgs a;
   int rc = make_args(a, grid, cta_pair, w_packed, n_out, n_units, k, m_tok, bn, epilogue, out, ld_out, ws, max_segs,
-                     amax_val, amax_idx, m_cap, prefetch, prefetch_bytes, prefetch_span, fix_counters, fix_units,
-                     n_fix);
+                     amax_val, amax_idx, m_cap, prefetch, prefetch_bytes, prefetch_span, fix_mode, fix_counters,
+                     fix_units, n_fix);
   if (rc) return rc;
   auto tx = reinterpret_cast<const CUtensorMap*>(tmap_x);
   auto st = reinterpret_cast<cudaStream_t>(stream);
@@ -1655,12 +1712,12 @@ extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, i
                                      int m_tok, int bn, int grid, int cta_pair, float* resid, float* ws, int max_segs, int m_cap,
                                      const void* prefetch, unsigned long long prefetch_bytes,
                                      unsigned long long prefetch_span, const void* norm_w, void* xn, float eps,
-                                     int* row_counters, int split_norm, int* fix_counters, const int* fix_units,
-                                     int n_fix, void* stream) {
+                                     int* row_counters, int split_norm, int fix_mode, int* fix_counters,
+                                     const int* fix_units, int n_fix, void* stream) {
   GemmArgs a;
   int rc = make_args(a, grid, cta_pair, w_packed, n_out, n_units, k, m_tok, bn, EPI_RESID_ADD_F32, resid, n_out, ws,
-                     max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes, prefetch_span, fix_counters,
-                     fix_units, n_fix);
+                     max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes, prefetch_span, fix_mode,
+                     fix_counters, fix_units, n_fix);
   if (rc) return rc;
   if (n_out % 8 || n_out > 256 * 4 * NORM_V4) return (int)cudaErrorInvalidValue;
   NormArgs na{reinterpret_cast<const bf16*>(norm_w), reinterpret_cast<bf16*>(xn), row_counters,
@@ -1670,7 +1727,7 @@ extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, i
   // split_norm: finish split units with the plain reduce kernel and normalise in
   // a separate row-parallel kernel (measured better when nothing overlaps the
   // arrival chain: one micro-batch in flight)
-  if (a.fused) {   // residual add and the next norm happen inside the GEMM kernel
+  if (a.fix_mode == FIX_FUSED) {   // residual add and the next norm happen inside the GEMM kernel
     a.post = POST_RESID_NORM;
     return dispatch_bn(bn, [&](auto c) {
       return launch_any<decltype(c)::value>(cta_pair, tx, a, grid, st, POST_RESID_NORM, &na);
@@ -1689,16 +1746,16 @@ extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, i
 extern "C" int pm_gemm_qkv_rope(const void* w_packed, const void* tmap_x, int n_out, int n_units, int k, int m_tok,
                                 int bn, int grid, int cta_pair, void* qkv_out, float* ws, int max_segs, int m_cap,
                                 const void* prefetch, unsigned long long prefetch_bytes,
-                                unsigned long long prefetch_span, int* fix_counters, const int* fix_units, int n_fix,
-                                void* q_out, void* pool,
+                                unsigned long long prefetch_span, int fix_mode, int* fix_counters,
+                                const int* fix_units, int n_fix, void* q_out, void* pool,
                                 const int* block_table, const int* positions, const float* rope, const void* qn_w,
                                 const void* kn_w, int H, int Hkv, int hd, int layer, int L_s, int max_blocks,
                                 float eps, void* stream) {
   GemmArgs a;
   int rc = make_args(a, grid, cta_pair, w_packed, n_out, n_units, k, m_tok, bn, EPI_STORE_BF16, qkv_out, n_out, ws,
-                     max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes, prefetch_span, fix_counters,
-                     fix_units, n_fix);
-  if (a.fused) a.post = POST_QKV_ROPE;
+                     max_segs, nullptr, nullptr, m_cap, prefetch, prefetch_bytes, prefetch_span, fix_mode,
+                     fix_counters, fix_units, n_fix);
+  a.post = POST_QKV_ROPE;   // every unit arrives in FIX_POLL / FIX_FUSED
   if (rc) return rc;
   if (n_out != (H + 2 * Hkv) * hd || (hd != 64 && hd != 128) || UNIT_ROWS % hd) return (int)cudaErrorInvalidValue;
   RopeArgs ra{reinterpret_cast<bf16*>(q_out), reinterpret_cast<bf16*>(pool), block_table, positions, rope,

@@ -122,6 +122,8 @@ class DecodeEngine:
         self.pp = pp
         if lanes is None:
             lanes = 2 if (pp == 1 and local_stages is None) else 1
+            if _os.environ.get("PM_LANES"):   # A/B and debugging
+                lanes = int(_os.environ["PM_LANES"])
         for s in (range(pp) if local_stages is None else local_stages):
             ex = StageExecutor(spec, stage_layers(spec, pp, s), first=(s == 0), last=(s == pp - 1),
                                m_cap=self.m_cap, pool_blocks=pool_blocks, max_blocks=self.max_blocks,

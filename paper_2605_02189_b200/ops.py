@@ -96,6 +96,15 @@ def bn_for(m_tok: int) -> int:
 
 
 EPI_STORE_BF16, EPI_RESID_ADD, EPI_SILU_MUL, EPI_LOGITS_ARGMAX = 0, 1, 2, 3
+# how split stream-K units are finished (pm_gemm's fix_mode): post kernel after the
+# whole GEMM grid / in-kernel tasks / post kernel polling per-unit arrivals.
+# FIX_POLL is opt-in (PM_FIX_POLL=1) and NOT for CUDA-graph replays: eager launches
+# are bit-identical to FIX_POST (tests/test_fused_fixup_gpu.py) and the per-stage
+# benches gain ~0.5-1 %, but engine steps replayed from CUDA graphs with programmatic
+# dependent launch produce wrong logits (correct with graphs and PDL off, or eager
+# with PDL on) -- profiles/r2/fused_fixup.md.
+FIX_POST, FIX_FUSED, FIX_POLL = 0, 1, 2
+FIX_POLL_ON = __import__("os").environ.get("PM_FIX_POLL", "0") == "1"
 UNIT_ROWS = 256
 
 
@@ -303,12 +312,15 @@ class Linear:
         self.fused = True
 
     def _fixargs(self, m_tok, ws, qkv=False):
-        """(counters, unit list, count) of an in-kernel fixup launch, or nulls
-        (post kernel) when not fused or the step spans several token tiles."""
-        if not self.fused or self.plan(m_tok)[3] != 1:
-            return None, None, 0
-        lst, n = self._fix[qkv]
-        return C.c_void_p(ws.fix_cnt.data_ptr()), C.c_void_p(lst.data_ptr()), n
+        """(mode, counters, unit list, count) of a launch: the in-kernel fixup
+        when fused (one token tile), else the post kernels polling per-unit
+        arrivals (FIX_POLL) unless PM_FIX_POLL=0."""
+        if self.fused and self.plan(m_tok)[3] == 1:
+            lst, n = self._fix[qkv]
+            return FIX_FUSED, C.c_void_p(ws.fix_cnt.data_ptr()), C.c_void_p(lst.data_ptr()), n
+        if FIX_POLL_ON and self.plan(m_tok)[3] == 1:   # counters sized for one token tile
+            return FIX_POLL, C.c_void_p(ws.fix_cnt.data_ptr()), None, 0
+        return FIX_POST, None, None, 0
 
     def launches(self, m_tok) -> int:
         """Kernels one call launches: the stream-K GEMM, plus gemm_reduce when

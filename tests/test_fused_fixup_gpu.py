@@ -198,3 +198,61 @@ def test_fused_in_cuda_graph_replays():
         outs.append((resid.clone(), xn[:m].clone(), act[:m].clone()))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("name,n_out,k,m,epi,sms", PLAIN, ids=[p[0] for p in PLAIN])
+def test_polling_post_kernels_equal_grid_wait(name, n_out, k, m, epi, sms, monkeypatch):
+    """FIX_POLL (post-kernel CTAs start on their unit's arrivals) == FIX_POST
+    (post kernel waits for the whole GEMM grid), bit for bit, counters re-armed."""
+    g = torch.Generator(device=DEV).manual_seed(n_out + k + m + 1)
+    w = (torch.randn(n_out, k, generator=g, device=DEV) * 0.05).to(torch.bfloat16)
+    m_cap = 256
+    x = torch.zeros(m_cap, k, device=DEV, dtype=torch.bfloat16)
+    x[:m] = torch.randn(m, k, generator=g, device=DEV).to(torch.bfloat16)
+    maps = ops.activation_maps(x)
+    width = n_out // 2 if epi == ops.EPI_SILU_MUL else n_out
+    dt = torch.float32 if epi in (ops.EPI_RESID_ADD, ops.EPI_LOGITS_ARGMAX) else torch.bfloat16
+    y0 = torch.randn(m_cap, width, generator=g, device=DEV).to(dt)
+    outs = []
+    for poll in (False, True):
+        monkeypatch.setattr(ops, "FIX_POLL_ON", poll)
+        lin = ops.Linear(w)
+        lin.sms = sms
+        ws = _ws(m_cap, lin)
+        y = y0.clone()
+        ids = torch.full((m_cap,), -1, dtype=torch.int32, device=DEV)
+        for _ in range(2):
+            lin(maps, m, epi, y, width, ws)
+            if epi == ops.EPI_LOGITS_ARGMAX:
+                ops.argmax_reduce(ws, lin.n_units, m, ids)
+        torch.cuda.synchronize()
+        assert (ws.fix_cnt == 0).all()
+        outs.append((y.cpu(), ids.cpu()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("split_norm", [False, True])
+@pytest.mark.parametrize("name,d,k,m,sms", RESID[:4], ids=[r[0] for r in RESID[:4]])
+def test_polling_resid_norm_and_qkv_equal_grid_wait(name, d, k, m, sms, split_norm, monkeypatch):
+    g = torch.Generator(device=DEV).manual_seed(d + k + m + 3)
+    w = (torch.randn(d, k, generator=g, device=DEV) * 0.05).to(torch.bfloat16)
+    m_cap = 256
+    x = torch.zeros(m_cap, k, device=DEV, dtype=torch.bfloat16)
+    x[:m] = torch.randn(m, k, generator=g, device=DEV).to(torch.bfloat16)
+    nw = (1 + 0.1 * torch.randn(d, generator=g, device=DEV)).to(torch.bfloat16)
+    maps = ops.activation_maps(x)
+    r0 = torch.randn(m_cap, d, generator=g, device=DEV)
+    outs = []
+    for poll in (False, True):
+        monkeypatch.setattr(ops, "FIX_POLL_ON", poll)
+        lin = ops.Linear(w)
+        lin.sms = sms
+        ws = _ws(m_cap, lin)
+        r = r0.clone()
+        xn = torch.zeros(m_cap, d, device=DEV, dtype=torch.bfloat16)
+        for _ in range(2):
+            lin.resid_rmsnorm(maps, m, r, ws, nw, xn, 1e-6, split_norm=split_norm)
+        torch.cuda.synchronize()
+        assert (ws.fix_cnt == 0).all() and (ws.row_cnt == 0).all()
+        outs.append((r.cpu(), xn[:m].cpu()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])

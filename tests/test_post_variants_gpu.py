@@ -58,7 +58,7 @@ torch.save(out, sys.argv[1])
 
 def _run(tmp_path, scalar):
     path = str(tmp_path / f"post_{scalar}.pt")
-    env = dict(os.environ, PM_POST_SCALAR=str(scalar))
+    env = dict(os.environ, PM_POST_SCALAR=str(scalar), PM_FIX_POLL="0")   # scalar kernels do not poll
     subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT), path], env=env, check=True, timeout=600)
     return torch.load(path)
 
