@@ -491,6 +491,8 @@ def stage_summary(config, steps, warmup, peaks, local, calibrate=True):
     eng, _, spec, reqs, params, desc = build_engine(config, local=local, calibrate=calibrate)
     for _ in range(warmup):
         assert eng.step() is not None
+    if calibrate:   # closed loop: the warm-up steps' measured periods correct the fit
+        eng.refit_online()
     r = measure_device(eng, steps, peaks, local)
     out = {"config": config, "workload": desc["workload"], "tokens_per_s": r["value"],
            "ms_per_step": r["ms_per_step"], "rows_per_step": r["rows_per_step"],
@@ -520,6 +522,8 @@ def run_ours(args):
                                                        calibrate=args.calibrate and world == 1)
     for _ in range(args.warmup):
         assert eng.step() is not None
+    if args.calibrate and world == 1:   # closed loop: the warm-up steps' periods correct the fit
+        eng.refit_online()
     torch.cuda.synchronize()
     dev = measure_device(eng, args.steps, peaks, local, dist)
     e2e = measure_e2e(eng, args.steps, dist)

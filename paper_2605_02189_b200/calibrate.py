@@ -86,6 +86,21 @@ def calibrate_on_device(engine, grid=None, reps: int = 5, pipelined: bool = None
     return params, samples, err
 
 
+def step_errors(records):
+    """(predicted, measured) step seconds of consecutive recorded steps: the
+    planner's predicted step time vs the period end(t) - end(t-1)."""
+    recs = sorted((r for r in records if "end" in r and r.get("info", {}).get("plan") is not None),
+                  key=lambda r: r["t"])
+    out = []
+    for prev, cur in zip(recs, recs[1:]):
+        if cur["t"] != prev["t"] + 1:
+            continue
+        meas = prev["end"].elapsed_time(cur["end"]) * 1e-3
+        if meas > 0:
+            out.append((cur["info"]["plan"].predicted_exec_seconds, meas))
+    return out
+
+
 def step_fidelity(records, t0: int = 0):
     """Per-step estimator fidelity of a decode run (the paper's claim, PAPER.md
     667-669): the planner's predicted step time vs the measured step period

@@ -224,8 +224,12 @@ class DecodeEngine:
 
     def _upload_meta(self, rows, positions, tables, stream=None, lane=0):
         """Block tables, positions, seq lens and slots of the step's rows,
-        padded to the 16-row bucket with rows aimed at the trash block/slot."""
+        padded to the 16-row bucket with rows aimed at the trash block/slot.
+        Returns the physical blocks the step reads / writes (the KV engine's
+        block-hazard record: a later prefetch into one of them must wait for
+        this step's compute)."""
         self._fill_meta([tables[r] for r in rows], positions, [self.slot_of[r] for r in rows], stream, lane)
+        return self._last_used_blocks
 
     def _upload_meta_rows(self, table, positions, M=None, last_slot=None, stream=None):
         """Prefill chunk: every row is a token of one request (its block
@@ -318,6 +322,24 @@ class DecodeEngine:
         self.calibration = {"params": params, "samples": samples, "max_rel_fit_err": err}
         torch.cuda.synchronize()
         return params
+
+    def refit_online(self, skip: int = 2):
+        """Closed loop on the running engine: the planner's predicted step time
+        vs the measured step period of the steps run so far (CUDA events, this
+        engine's lane mode and transfer load included) -> shift delta by the
+        median error, so the prefetch budget B * T_hat follows the box.  alpha and
+        beta keep the on-box grid fit (the running steps span too little of
+        (b, L) to refit them).  Returns the shift in seconds."""
+        from .calibrate import step_errors
+        torch.cuda.synchronize()
+        pairs = step_errors(self.stages[0][1].records)[skip:]
+        if len(pairs) < 4:
+            return 0.0
+        shift = float(np.median([meas - pred for pred, meas in pairs]))
+        p = self.params
+        self.params = EstimatorParams(p.alpha, p.beta, max(p.delta + shift, 1e-6))
+        self.control.params = self.params
+        return shift
 
     def _hop_buffer(self, lane, resid):
         """bf16 wire buffer of the single-process stage hop (one per lane)."""

@@ -257,7 +257,7 @@ class GemmWorkspace:
     """Stream-K partials, per-row counters and argmax partials shared by all
     projections of one executor (launches on one stream run in order)."""
 
-    def __init__(self, m_cap: int, ws_floats: int, max_units: int, vocab_units: int, device):
+    def __init__(self, m_cap: int, ws_floats: int, max_units: int, vocab_units: int, device, sites: int = 1):
         self.m_cap = m_cap
         self.ws = torch.empty(max(1, ws_floats), dtype=torch.float32, device=device)
         # one argmax tile per 128-row half of a vocabulary unit
@@ -265,8 +265,16 @@ class GemmWorkspace:
         self.amax_idx = torch.empty(2 * max(1, vocab_units) * m_cap, dtype=torch.int32, device=device)
         # per-row arrival counts of the fused residual + RMSNorm epilogue; kernels leave them zero
         self.row_cnt = torch.zeros(m_cap, dtype=torch.int32, device=device)
-        # per-unit segment arrivals + finished tasks of the in-kernel fixup (Linear.fused); left zero
-        self.fix_cnt = torch.zeros(2 * max(1, max_units, vocab_units), dtype=torch.int32, device=device)
+        # per-unit segment arrivals + readers / finished tasks of FIX_POLL / FIX_FUSED launches; left
+        # zero.  One slice per GEMM call site of a step (``sites``): a polling post kernel may start
+        # before the previous projection's post kernel has re-armed ITS counts, so consecutive
+        # projections must not share a slice
+        self.fix_stride = 2 * max(1, max_units, vocab_units)
+        self.fix_cnt = torch.zeros(self.fix_stride * max(1, sites), dtype=torch.int32, device=device)
+
+    def fix_ptr(self, site: int = 0):
+        assert 0 <= site < self.fix_cnt.numel() // self.fix_stride, "GEMM call site out of range"
+        return C.c_void_p(self.fix_cnt.data_ptr() + 4 * self.fix_stride * site)
 
     @staticmethod
     def floats_needed(linears, m_cap):
@@ -311,15 +319,15 @@ class Linear:
         self._fix = {False: (split, n), True: (every, self.n_units)}
         self.fused = True
 
-    def _fixargs(self, m_tok, ws, qkv=False):
+    def _fixargs(self, m_tok, ws, qkv=False, site=0):
         """(mode, counters, unit list, count) of a launch: the in-kernel fixup
         when fused (one token tile), else the post kernels polling per-unit
         arrivals (FIX_POLL) unless PM_FIX_POLL=0."""
         if self.fused and self.plan(m_tok)[3] == 1:
             lst, n = self._fix[qkv]
-            return FIX_FUSED, C.c_void_p(ws.fix_cnt.data_ptr()), C.c_void_p(lst.data_ptr()), n
+            return FIX_FUSED, ws.fix_ptr(site), C.c_void_p(lst.data_ptr()), n
         if FIX_POLL_ON and self.plan(m_tok)[3] == 1:   # counters sized for one token tile
-            return FIX_POLL, C.c_void_p(ws.fix_cnt.data_ptr()), None, 0
+            return FIX_POLL, ws.fix_ptr(site), None, 0
         return FIX_POST, None, None, 0
 
     def launches(self, m_tok) -> int:
@@ -351,12 +359,12 @@ class Linear:
             TIMER.around("gemm", kind_bytes, stream, go, split=True)
 
     def __call__(self, x_maps: dict, m_tok: int, epilogue: int, out, ld_out: int, ws: GemmWorkspace,
-                 stream=None, prefetch=None):
+                 stream=None, prefetch=None, site: int = 0):
         """``prefetch``: optional (tensor, nbytes) the next operation reads
         first; the kernel pulls it into L2 while it drains."""
         bn, grid, segs, tt, pair = self.plan(m_tok)
         pf_ptr, pf_bytes, pf_span = self._pf(prefetch)
-        fx = self._fixargs(m_tok, ws)
+        fx = self._fixargs(m_tok, ws, site=site)
 
         def go():
             _C.call("pm_gemm", _ptr(self.packed), x_maps[bn // 2 if pair else bn].ptr, self.n_out, self.n_units, self.k, m_tok, bn,
@@ -367,12 +375,12 @@ class Linear:
         self._timed(self.weight_bytes + m_tok * self.k * 2 + m_tok * self.n_out * out_b, stream, go)
 
     def resid_rmsnorm(self, x_maps: dict, m_tok: int, resid, ws: GemmWorkspace, norm_w, xn, eps: float,
-                      stream=None, prefetch=None, split_norm: bool = False):
+                      stream=None, prefetch=None, split_norm: bool = False, site: int = 0):
         """resid += x W^T, then xn = RMSNorm(resid) * norm_w -- the residual
         projection fused with the next layer norm (pm_gemm_resid_rmsnorm)."""
         bn, grid, segs, tt, pair = self.plan(m_tok)
         pf_ptr, pf_bytes, pf_span = self._pf(prefetch)
-        fx = self._fixargs(m_tok, ws)
+        fx = self._fixargs(m_tok, ws, site=site)
 
         def go():
             _C.call("pm_gemm_resid_rmsnorm", _ptr(self.packed), x_maps[bn // 2 if pair else bn].ptr, self.n_out, self.n_units, self.k,
@@ -412,12 +420,12 @@ class Linear:
                 _stream(stream))
 
     def qkv_rope(self, x_maps: dict, m_tok: int, qkv, ws: GemmWorkspace, q_out, pool, block_table, positions,
-                 rope, qn_w, kn_w, H, Hkv, hd, layer, L_s, eps, stream=None, prefetch=None):
+                 rope, qn_w, kn_w, H, Hkv, hd, layer, L_s, eps, stream=None, prefetch=None, site: int = 0):
         """QKV projection fused with q/k RMSNorm + RoPE + paged KV append
         (pm_gemm_qkv_rope); ``qkv`` is scratch for units left whole."""
         bn, grid, segs, tt, pair = self.plan(m_tok)
         pf_ptr, pf_bytes, pf_span = self._pf(prefetch)
-        fx = self._fixargs(m_tok, ws, qkv=True)
+        fx = self._fixargs(m_tok, ws, qkv=True, site=site)
 
         def go():
             _C.call("pm_gemm_qkv_rope", _ptr(self.packed), x_maps[bn // 2 if pair else bn].ptr, self.n_out, self.n_units, self.k,

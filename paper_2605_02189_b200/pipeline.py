@@ -236,7 +236,12 @@ class PipelineRank:
         ctx = torch.cuda.stream(self.stream) if self.stream is not None else _Null()
         with ctx:
             if self.upload_meta is not None:
-                self.upload_meta(work.rows, work.positions, work.tables)
+                used = self.upload_meta(work.rows, work.positions, work.tables)
+                if used is not None:
+                    # blocks this step touches: a later prefetch into one of them waits
+                    # for this step's compute (without it an H2D copy could overwrite KV
+                    # an in-flight step still reads)
+                    rec["used_blocks"] = used
             if self.kv is not None:
                 self.kv.before_compute(t, work, rec)
             if self.first and self.world > 1:

@@ -124,8 +124,10 @@ class StageExecutor:
         lins = [x[k] for x in self.W for k in ("qkv", "o", "gu", "down")] + ([self.lm_head] if self.last else [])
         for lin in lins:   # before the workspace is sized from the plans
             lin.sms = self.gemm_sms
+        # one fixup-counter slice per GEMM call site of a step (4 per layer + lm_head)
         self.gws = ops.GemmWorkspace(m_cap, ops.GemmWorkspace.floats_needed(lins, m_cap),
-                                     max(l.n_units for l in lins), self.lm_head.n_units if self.last else 1, device)
+                                     max(l.n_units for l in lins), self.lm_head.n_units if self.last else 1, device,
+                                     sites=4 * self.L_s + 1)
         self.aws = ops.AttnWorkspace(m_cap, s.Hkv, s.hd, self.max_blocks, device, rows_hint=self.rows_hint)
 
     def enable_fused(self):
@@ -193,25 +195,27 @@ class StageExecutor:
             # QKV projection + q/k norm + RoPE + paged KV append (one fused epilogue)
             w["qkv"].qkv_rope(self.xn_maps, M, self.qkv, self.gws, self.q, self.pool, self.block_table,
                               self.positions, self.rope, w["q_norm"], w["k_norm"], s.H, s.Hkv, s.hd, li, self.L_s,
-                              s.eps, stream, prefetch=pf(w["o"]) if PF_QKV else None)
+                              s.eps, stream, prefetch=pf(w["o"]) if PF_QKV else None, site=4 * li)
             if layer_hook is not None:   # layer li's K/V is in the pool (prefill offload)
                 layer_hook(li)
             ops.paged_attention(self.pool_map, self.q, self.block_table, self.seq_lens, self.attn, self.aws,
                                 M, s.H, s.Hkv, s.hd, li, self.L_s, stream, kv_tokens=kv_tokens)
             # O projection + residual + post-attention RMSNorm
             w["o"].resid_rmsnorm(self.attn_maps, M, self.resid, self.gws, w["mlp_norm"], self.xn, s.eps, stream,
-                                 split_norm=self.split_norm, prefetch=pf(w["gu"]))
-            w["gu"](self.xn_maps, M, ops.EPI_SILU_MUL, self.act, s.ffn, self.gws, stream, prefetch=pf(w["down"]))
+                                 split_norm=self.split_norm, prefetch=pf(w["gu"]), site=4 * li + 1)
+            w["gu"](self.xn_maps, M, ops.EPI_SILU_MUL, self.act, s.ffn, self.gws, stream, prefetch=pf(w["down"]),
+                    site=4 * li + 2)
             # down projection + residual + the next norm (next layer's, or the final one)
             nxt = self.W[li + 1]["attn_norm"] if li + 1 < len(self.W) else (self.final_norm if self.last else None)
             nxt_lin = nxt_w["qkv"] if nxt_w is not None else (self.lm_head if self.last else None)
             if nxt is not None:
                 w["down"].resid_rmsnorm(self.act_maps, M, self.resid, self.gws, nxt, self.xn, s.eps, stream,
-                                        split_norm=self.split_norm, prefetch=pf(nxt_lin))
+                                        split_norm=self.split_norm, prefetch=pf(nxt_lin), site=4 * li + 3)
             else:
-                w["down"](self.act_maps, M, ops.EPI_RESID_ADD, self.resid, s.d, self.gws, stream)
+                w["down"](self.act_maps, M, ops.EPI_RESID_ADD, self.resid, s.d, self.gws, stream, site=4 * li + 3)
         if self.last:
-            self.lm_head(self.xn_maps, M, ops.EPI_LOGITS_ARGMAX, self.logits, s.vocab, self.gws, stream)
+            self.lm_head(self.xn_maps, M, ops.EPI_LOGITS_ARGMAX, self.logits, s.vocab, self.gws, stream,
+                         site=4 * self.L_s)
             ops.argmax_reduce(self.gws, self.lm_head.n_units, M, self.out_ids, self.tok_table, self.slots, stream)
 
     def _forward_cl(self, M: int, stream, prefill_tokens: bool, layer_hook):

@@ -148,9 +148,13 @@ def test_fused_qkv_rope_equals_post_kernel(name, H, Hkv, hd, k, m, qk_norm, sms)
         assert (ws_f.fix_cnt == 0).all(), (name, rep)
 
 
-def test_fused_in_cuda_graph_replays():
-    """A graph of back-to-back fused projections (counters shared through one
-    workspace) replays to the same result as eager post-kernel launches."""
+@pytest.mark.parametrize("mode", ["fused", "poll"])
+def test_fused_in_cuda_graph_replays(mode, monkeypatch):
+    """A graph of back-to-back projections with programmatic dependent launch
+    -- in-kernel fixups (counters shared through one workspace), or polling
+    post kernels (one counter slice per call site: a polling post kernel may
+    start before the previous projection's post kernel re-armed its counts)
+    -- replays to the same result as eager grid-wait launches."""
     g = torch.Generator(device=DEV).manual_seed(5)
     d, ffn, m, m_cap = 5120, 25600, 48, 256
     w_o = (torch.randn(d, 8192, generator=g, device=DEV) * 0.02).to(torch.bfloat16)
@@ -162,12 +166,14 @@ def test_fused_in_cuda_graph_replays():
     resid0 = torch.randn(m_cap, d, generator=g, device=DEV)
     outs = []
     for fused in (False, True):
+        monkeypatch.setattr(ops, "FIX_POLL_ON", fused and mode == "poll")
         lins = [ops.Linear(w) for w in (w_o, w_gu, w_dn)]
         for lin in lins:
             lin.sms = 116
-            if fused:
+            if fused and mode == "fused":
                 lin.enable_fused(DEV)
-        ws = ops.GemmWorkspace(m_cap, ops.GemmWorkspace.floats_needed(lins, m_cap), max(l.n_units for l in lins), 1, DEV)
+        ws = ops.GemmWorkspace(m_cap, ops.GemmWorkspace.floats_needed(lins, m_cap), max(l.n_units for l in lins), 1, DEV,
+                               sites=3)
         resid = resid0.clone()
         xn = torch.zeros(m_cap, d, device=DEV, dtype=torch.bfloat16)
         act = torch.zeros(m_cap, ffn, device=DEV, dtype=torch.bfloat16)
@@ -175,9 +181,9 @@ def test_fused_in_cuda_graph_replays():
         st = torch.cuda.Stream()
 
         def chain():
-            lins[0].resid_rmsnorm(atm, m, resid, ws, nw, xn, 1e-6, st, split_norm=True)
-            lins[1](xm, m, ops.EPI_SILU_MUL, act, ffn, ws, st)
-            lins[2].resid_rmsnorm(am, m, resid, ws, nw, xn, 1e-6, st, split_norm=True)
+            lins[0].resid_rmsnorm(atm, m, resid, ws, nw, xn, 1e-6, st, split_norm=True, site=0)
+            lins[1](xm, m, ops.EPI_SILU_MUL, act, ffn, ws, st, site=1)
+            lins[2].resid_rmsnorm(am, m, resid, ws, nw, xn, 1e-6, st, split_norm=True, site=2)
         if fused:
             with torch.cuda.stream(st):
                 chain()   # warm-up (attributes)
@@ -187,8 +193,8 @@ def test_fused_in_cuda_graph_replays():
             with torch.cuda.graph(gr, stream=st):
                 chain()
             for _ in range(3):
-                resid.copy_(resid0)
                 with torch.cuda.stream(st):
+                    resid.copy_(resid0)
                     gr.replay()
                 torch.cuda.synchronize()
         else:
