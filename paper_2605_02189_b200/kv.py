@@ -51,6 +51,8 @@ if os.environ.get("PM_OFFLOAD_DMA") == "0":
     OFFLOAD_MODE = "kernel"
 OFFLOAD_CTAS = int(os.environ.get("PM_OFFLOAD_CTAS", "32"))
 STAGE_RING = 4   # gather-offload staging slabs (steps in flight on the D2H stream)
+# A/B: lanes at staggered stream priorities (lane 0 first for free SMs) instead of equal ones
+LANE_PRIO_STAGGER = os.environ.get("PM_LANE_PRIO", "flat") == "stagger"
 
 
 def device_numa_node(device=None) -> int:
@@ -92,6 +94,7 @@ class HostReplica:
 
     def close(self):
         if self.ptr:
+            torch.cuda.synchronize()   # no copy may still read or write the pages being unpinned
             _C.call("pm_host_free_numa", _C.C.c_void_p(self.ptr), self.nbytes, self.numa_node)
             self.ptr = None
 
@@ -217,7 +220,11 @@ class KvEngine:
         return len(dst) * bb
 
     def add_lane(self) -> int:
-        self.streams.append(torch.cuda.Stream(device=self.dev, priority=self._compute_prio))
+        prio = self._compute_prio
+        if LANE_PRIO_STAGGER:   # lane i one priority level below lane i - 1 (still above the copies)
+            lo, hi = torch.cuda.Stream.priority_range()
+            prio = min(lo, self._compute_prio + len(self.streams)) if hi < lo else self._compute_prio
+        self.streams.append(torch.cuda.Stream(device=self.dev, priority=prio))
         self.block_last_compute.append(np.full(self.ex.pool_blocks, -1, dtype=np.int64))
         return len(self.streams) - 1
 

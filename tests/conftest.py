@@ -21,3 +21,16 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _drain_device_between_tests(request):
+    """After each GPU test, wait for every stream before the next test runs:
+    an engine's copy streams (KV prefetch H2D, offload D2H, host scatters)
+    may still be in flight when its tensors go out of scope, and the caching
+    allocator would hand the same device memory to the next test's engine."""
+    yield
+    if "gpu" in request.keywords:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
