@@ -279,6 +279,31 @@ def build_engine(config, rank=0, world=1, local=0, calibrate=True):
     return eng, None, spec, reqs, params, desc
 
 
+_PCIE = {}
+
+
+def pcie_peak(local=0):
+    """(H2D, D2H) bytes/s of a 256 MB pinned <-> device copy on this box
+    (best of 3, CUDA events; measured once per process)."""
+    import torch
+    if local not in _PCIE:
+        n = 256 << 20
+        host = torch.empty(n, dtype=torch.uint8).pin_memory()
+        dev = torch.empty(n, dtype=torch.uint8, device=f"cuda:{local}")
+        best = [0.0, 0.0]
+        for _ in range(3):
+            for k, (dst, src) in enumerate(((dev, host), (host, dev))):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                dst.copy_(src, non_blocking=True)
+                b.record()
+                torch.cuda.synchronize()
+                best[k] = max(best[k], n / (a.elapsed_time(b) * 1e-3))
+        _PCIE[local] = tuple(best)
+        del host, dev
+    return _PCIE[local]
+
+
 def measure_device(eng, steps, peaks, local=0, dist=None):
     """K pipelined steps through the engine (the host control plane runs
     ahead of the GPU), CUDA events on the compute stream, barrier +
@@ -327,7 +352,11 @@ def measure_device(eng, steps, peaks, local=0, dist=None):
     t_hbm = hbm_bytes / (peaks["hbm_gbs"] * 1e9)
     bw_h2d = h2d_b / h2d_busy if h2d_busy > 0 else None
     bw_d2h = d2h_b / d2h_busy if d2h_busy > 0 else None
-    t_pcie = max((h2d_b / steps) / bw_h2d if bw_h2d else 0.0, (d2h_b / steps) / bw_d2h if bw_d2h else 0.0)
+    # the PCIe side of the roofline uses the LINK's rate per direction (a large
+    # pinned copy measured on this box, pcie_peak()), not this run's achieved
+    # copy rates -- a slow offload path must not make the roofline easier
+    pk_h2d, pk_d2h = pcie_peak(local)
+    t_pcie = max((h2d_b / steps) / pk_h2d, (d2h_b / steps) / pk_d2h)
     roof_tok_s = M_avg / max(t_hbm, t_pcie)
     value = tokens / dev_s
     return {
@@ -340,8 +369,10 @@ def measure_device(eng, steps, peaks, local=0, dist=None):
         "decode_roofline": {"hbm_bytes_per_step": hbm_bytes, "t_hbm_ms": t_hbm * 1e3, "t_pcie_ms": t_pcie * 1e3,
                             "roofline_tok_s": roof_tok_s, "frac": value / roof_tok_s,
                             "peak_hbm_gbs": peaks["hbm_gbs"],
+                            "pcie_peak_GBps": {"h2d": pk_h2d / 1e9, "d2h": pk_d2h / 1e9},
                             "note": "per step: weights once + the active micro-batch's KV + new KV + activations "
-                                    "over HBM vs prefetch/offload bytes over PCIe at this run's measured rates"},
+                                    "over HBM (measured peak) vs prefetch / offload bytes over the PCIe link "
+                                    "(a 256 MB pinned copy per direction on this box)"},
     }
 
 
@@ -522,7 +553,7 @@ def run_ours(args):
                                                        calibrate=args.calibrate and world == 1)
     for _ in range(args.warmup):
         assert eng.step() is not None
-    if args.calibrate and world == 1:   # closed loop: the warm-up steps' periods correct the fit
+    if args.calibrate and world == 1:   # closed loop: the warm-up steps' measured periods correct the fit
         eng.refit_online()
     torch.cuda.synchronize()
     dev = measure_device(eng, args.steps, peaks, local, dist)

@@ -101,8 +101,12 @@ extern "C" int pm_host_alloc_numa(unsigned long long bytes, int numa_node, void*
   }
   cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
   if (e != cudaSuccess) {
+    // registering tens of GB of anonymous pages can fail on a loaded host (seen
+    // once as cudaErrorOperatingSystem): fall back to the driver's own pinned
+    // allocation, without the NUMA placement
     munmap(p, bytes);
-    return (int)e;
+    cudaGetLastError();
+    return (int)cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
   }
   *out = p;
   return 0;
@@ -110,8 +114,12 @@ extern "C" int pm_host_alloc_numa(unsigned long long bytes, int numa_node, void*
 extern "C" int pm_host_free_numa(void* p, unsigned long long bytes, int numa_node) {
   if (numa_node < 0) return (int)cudaFreeHost(p);
   cudaError_t e = cudaHostUnregister(p);
+  if (e != cudaSuccess) {   // the cudaHostAlloc fallback of pm_host_alloc_numa
+    cudaGetLastError();
+    return (int)cudaFreeHost(p);
+  }
   munmap(p, bytes);
-  return (int)e;
+  return 0;
 }
 
 // Device-side address of pinned host memory from pm_host_alloc (zero-copy reads).
