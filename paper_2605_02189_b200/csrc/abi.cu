@@ -8,6 +8,7 @@
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <thread>
 #include <vector>
 
@@ -54,17 +55,69 @@ extern "C" int pm_tmap_encode_2d(void* tmap_out, const void* gaddr, unsigned lon
 // Pitched copy (cudaMemcpy2DAsync): `height` rows of `width` bytes, row
 // strides dpitch / spitch -- one layer's K/V of a run of tokens between the
 // pool and the host replica (token stride = the pitch).
+// The pinned replica is registered in 1 GB pieces aligned to 1 GB (see
+// pm_host_alloc_numa) and a single cudaMemcpy may not span two registrations,
+// so host-side copies are cut at absolute 1 GB boundaries of either pointer
+// (harmless for device pointers).
+static constexpr unsigned long long PIN_CHUNK = 1ull << 30;
+static inline unsigned long long to_piece_end(const void* p) {
+  return PIN_CHUNK - (reinterpret_cast<unsigned long long>(p) & (PIN_CHUNK - 1));
+}
+static cudaError_t copy_1d(void* dst, const void* src, unsigned long long n, cudaStream_t st) {
+  while (n) {
+    const unsigned long long m = std::min(n, std::min(to_piece_end(dst), to_piece_end(src)));
+    cudaError_t e = cudaMemcpyAsync(dst, src, m, cudaMemcpyDefault, st);
+    if (e != cudaSuccess) return e;
+    dst = static_cast<char*>(dst) + m;
+    src = static_cast<const char*>(src) + m;
+    n -= m;
+  }
+  return cudaSuccess;
+}
+
 extern "C" int pm_copy_2d(void* dst, unsigned long long dpitch, const void* src, unsigned long long spitch,
                           unsigned long long width, unsigned long long height, void* stream) {
-  if (height == 0) return 0;
-  return (int)cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault,
-                                reinterpret_cast<cudaStream_t>(stream));
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  unsigned long long r = 0;
+  while (r < height) {
+    char* d = static_cast<char*>(dst) + r * dpitch;
+    const char* sp = static_cast<const char*>(src) + r * spitch;
+    const unsigned long long ed = to_piece_end(d), es = to_piece_end(sp);
+    cudaError_t e;
+    if (width > ed || width > es) {   // this row straddles a piece boundary
+      e = copy_1d(d, sp, width, st);
+      r += 1;
+    } else {   // rows that end before the next boundary on both sides
+      unsigned long long k = height - r;
+      k = std::min(k, (ed - width) / dpitch + 1);
+      k = std::min(k, (es - width) / spitch + 1);
+      e = cudaMemcpy2DAsync(d, dpitch, sp, spitch, width, k, cudaMemcpyDefault, st);
+      r += k;
+    }
+    if (e != cudaSuccess) return (int)e;
+  }
+  return 0;
 }
 
 // Pinned, portable host memory for the KV host replica (the paper's "CPU KV
 // pool").  The caller owns it and frees it with pm_host_free.
+// Pinning large host ranges fails intermittently on some boxes with
+// cudaErrorOperatingSystem (measured: 8-48 GB requests failing at random,
+// tools/diag_pinned.sh), so pinned allocations retry, and the replica is pinned
+// in 1 GB pieces (each retried) rather than as one multi-GB registration.
+static cudaError_t host_alloc_retry(void** out, unsigned long long bytes) {
+  cudaError_t e = cudaSuccess;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    e = cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+    if (e == cudaSuccess) return e;
+    cudaGetLastError();
+    usleep(20000 * (attempt + 1));
+  }
+  return e;
+}
+
 extern "C" int pm_host_alloc(unsigned long long bytes, void** out) {
-  return (int)cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+  return (int)host_alloc_retry(out, bytes);
 }
 // NUMA node of a CUDA device's PCIe attachment (sysfs), -1 when unknown.
 extern "C" int pm_device_numa_node(int device, int* node) {
@@ -87,26 +140,46 @@ extern "C" int pm_device_numa_node(int device, int* node) {
 
 // Pinned, mapped host memory placed on NUMA node `numa_node` (the node the
 // GPU's PCIe root hangs off, pm_device_numa_node): anonymous mmap, mbind
-// (MPOL_BIND) before first touch, then cudaHostRegister (portable | mapped).
-// numa_node < 0: plain pm_host_alloc.  Free with pm_host_free_numa.
+// (MPOL_BIND) before first touch, then cudaHostRegister (portable | mapped) in
+// 1 GB pieces, each retried.  If a piece cannot be pinned the range falls back
+// to cudaHostAlloc (no NUMA placement).  numa_node < 0: plain pm_host_alloc.
+// The range is contiguous and fully pinned either way; its mapped device
+// address (pm_host_device_ptr) covers the first piece only.  Free with
+// pm_host_free_numa.
 extern "C" int pm_host_alloc_numa(unsigned long long bytes, int numa_node, void** out) {
-  if (numa_node < 0) return (int)cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
-  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
-  if (p == MAP_FAILED) return (int)cudaErrorMemoryAllocation;
+  if (numa_node < 0) return (int)host_alloc_retry(out, bytes);
+  // reserve one piece more and trim, so the range starts on a 1 GB boundary
+  const unsigned long long page = 4096, len = (bytes + page - 1) / page * page;
+  void* raw = mmap(nullptr, len + PIN_CHUNK, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (raw == MAP_FAILED) return (int)host_alloc_retry(out, bytes);
+  const unsigned long long r0 = reinterpret_cast<unsigned long long>(raw);
+  const unsigned long long b0 = (r0 + PIN_CHUNK - 1) & ~(PIN_CHUNK - 1);
+  if (b0 > r0) munmap(raw, b0 - r0);
+  if (r0 + PIN_CHUNK > b0) munmap(reinterpret_cast<void*>(b0 + len), r0 + PIN_CHUNK - b0);
+  void* p = reinterpret_cast<void*>(b0);
   unsigned long mask[16] = {0};
   if (numa_node < 16 * 64) {
     mask[numa_node / 64] = 1ul << (numa_node % 64);
     // MPOL_BIND = 2; a failure (no NUMA support in the kernel / container) leaves the default policy
     syscall(SYS_mbind, p, bytes, 2, mask, (unsigned long)(16 * 64), 0u);
   }
-  cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
-  if (e != cudaSuccess) {
-    // registering tens of GB of anonymous pages can fail on a loaded host (seen
-    // once as cudaErrorOperatingSystem): fall back to the driver's own pinned
-    // allocation, without the NUMA placement
-    munmap(p, bytes);
-    cudaGetLastError();
-    return (int)cudaHostAlloc(out, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+  unsigned long long done = 0;
+  while (done < bytes) {
+    const unsigned long long n = bytes - done < PIN_CHUNK ? bytes - done : PIN_CHUNK;
+    cudaError_t e = cudaErrorUnknown;
+    for (int attempt = 0; attempt < 8 && e != cudaSuccess; ++attempt) {
+      e = cudaHostRegister(static_cast<char*>(p) + done, n, cudaHostRegisterPortable | cudaHostRegisterMapped);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        usleep(20000 * (attempt + 1));
+      }
+    }
+    if (e != cudaSuccess) {   // give the range back and use the driver's allocation instead
+      for (unsigned long long o = 0; o < done; o += PIN_CHUNK) cudaHostUnregister(static_cast<char*>(p) + o);
+      munmap(p, len);
+      return (int)host_alloc_retry(out, bytes);
+    }
+    done += n;
   }
   *out = p;
   return 0;
@@ -118,7 +191,8 @@ extern "C" int pm_host_free_numa(void* p, unsigned long long bytes, int numa_nod
     cudaGetLastError();
     return (int)cudaFreeHost(p);
   }
-  munmap(p, bytes);
+  for (unsigned long long o = PIN_CHUNK; o < bytes; o += PIN_CHUNK) cudaHostUnregister(static_cast<char*>(p) + o);
+  munmap(p, (bytes + 4095) / 4096 * 4096);
   return 0;
 }
 
@@ -317,7 +391,7 @@ extern "C" int pm_copy_pieces(void* dst_base, const void* src_base, const long l
     i = j;
   }
   for (size_t k = 0; k < dsts.size(); ++k) {
-    cudaError_t e = cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyDefault, st);
+    cudaError_t e = copy_1d(dsts[k], srcs[k], sizes[k], st);
     if (e != cudaSuccess) return (int)e;
   }
   return 0;

@@ -148,8 +148,11 @@ class DecodeEngine:
         self.lanes = lanes
         # one micro-batch in flight: nothing overlaps the fused norm's arrival
         # chain, and fixup + a row-parallel norm kernel measured faster
+        split = lanes == 1
+        if _os.environ.get("PM_SPLIT_NORM"):   # A/B
+            split = _os.environ["PM_SPLIT_NORM"] == "1"
         for ex, _ in self.stages:
-            ex.split_norm = lanes == 1
+            ex.split_norm = split
             if lanes == 1 and FUSED_FIXUP:
                 ex.enable_fused()
         self.lane_stages = [self.stages]

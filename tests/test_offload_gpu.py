@@ -54,3 +54,33 @@ def test_engine_replica_bit_exact_per_offload_mode(mode, monkeypatch):
         n += 1
     assert eng.n_evicted > 0 and eng.n_prefetched > 0
     check_replica(eng)
+
+
+def test_chunk_pinned_replica_copies_across_pieces():
+    """The replica is pinned in 1 GB pieces (pm_host_alloc_numa): copies that
+    straddle a piece boundary still move the right bytes, both directions."""
+    from paper_2605_02189_b200.kv import device_numa_node
+    nbytes = (2 << 30) + (64 << 20)
+    node = max(0, device_numa_node())
+    p = _C.C.c_void_p()
+    _C.call("pm_host_alloc_numa", nbytes, node, _C.C.byref(p))
+    try:
+        host = np.frombuffer((ctypes.c_uint8 * nbytes).from_address(p.value), dtype=np.uint8)
+        lo, n = (1 << 30) - (3 << 20), 6 << 20          # 3 MB each side of the first boundary
+        host[lo:lo + n] = np.random.default_rng(1).integers(0, 255, n, dtype=np.uint8)
+        dev = torch.empty(n, dtype=torch.uint8, device="cuda")
+        st = torch.cuda.Stream()
+        off = np.array([0], dtype=np.int64)
+        src = np.array([lo], dtype=np.int64)
+        _C.call("pm_copy_pieces", _C.C.c_void_p(dev.data_ptr()), p, off.ctypes.data_as(_C.C.c_void_p),
+                src.ctypes.data_as(_C.C.c_void_p), 1, n, _C.C.c_void_p(st.cuda_stream))
+        st.synchronize()
+        assert np.array_equal(dev.cpu().numpy(), host[lo:lo + n])
+        dev.add_(1)
+        dst = np.array([lo + (1 << 30)], dtype=np.int64)   # straddles the second boundary
+        _C.call("pm_copy_pieces", p, _C.C.c_void_p(dev.data_ptr()), dst.ctypes.data_as(_C.C.c_void_p),
+                off.ctypes.data_as(_C.C.c_void_p), 1, n, _C.C.c_void_p(st.cuda_stream))
+        st.synchronize()
+        assert np.array_equal(host[lo + (1 << 30):lo + (1 << 30) + n], dev.cpu().numpy())
+    finally:
+        _C.call("pm_host_free_numa", p, nbytes, node)
