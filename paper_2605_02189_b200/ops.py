@@ -132,10 +132,11 @@ PAIR_MAX_UNITS = int(__import__("os").environ.get("PM_PAIR_MAX_UNITS", "64"))   
 
 
 # SMs a decode GEMM's stream-K workers span.  Measured on the C2 bench
-# (two lanes in flight): 128 of the 148 SMs is ~1.5 % faster per step than
-# all of them -- the other lane's fixup / attention CTAs start on the 20 free
-# SMs instead of queueing behind the GEMM's drain (PM_GEMM_CTAS overrides).
-GEMM_CTAS = int(__import__("os").environ.get("PM_GEMM_CTAS", "128"))
+# (two lanes in flight, round 2, tools/ab_tune*.sh): 136 -> 5.50-5.55 ms/step,
+# 140 -> 5.55, 144 -> 5.80-5.85, 128 -> 5.81-5.88, 132 -> 5.96, 148 slower
+# still -- the other lane's fixup / attention CTAs start on the free SMs
+# instead of queueing behind the GEMM's drain (PM_GEMM_CTAS overrides).
+GEMM_CTAS = int(__import__("os").environ.get("PM_GEMM_CTAS", "136"))
 # ... and with a single micro-batch in flight (per-stage runs): measured C3
 # 2.140 -> 2.122 ms/step at 116 (PM_GEMM_CTAS_1LANE overrides)
 GEMM_CTAS_1LANE = int(__import__("os").environ.get("PM_GEMM_CTAS_1LANE", "116"))
