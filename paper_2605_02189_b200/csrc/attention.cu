@@ -472,7 +472,11 @@ int num_sms() {   // of the current device (cached per device)
   if (!sms[dev]) {
     int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (const char* e = getenv("PM_ATTN_SMS")) n = atoi(e);   // tuning experiments only
+    // the persistent attention grid spans ~81 % of the SMs (120 of 148): the
+    // next projection's CTAs land on the rest while attention drains (measured
+    // C2 5.52 -> 5.46 ms/step, C3 stage 1.925 -> 1.910; tools/ab_tune5/6.sh)
+    n = n * 120 / 148;
+    if (const char* e = getenv("PM_ATTN_SMS")) n = atoi(e);   // tuning override
     sms[dev] = n;
   }
   return sms[dev];
