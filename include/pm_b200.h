@@ -36,8 +36,10 @@ int pm_host_alloc(unsigned long long bytes, void** out);
 int pm_host_free(void* p);
 /* NUMA node of device `device`'s PCIe attachment (sysfs; -1 unknown) */
 int pm_device_numa_node(int device, int* node);
-/* pinned + mapped host memory bound to NUMA node `numa_node` (mmap + mbind + cudaHostRegister; < 0: pm_host_alloc);
- * free with pm_host_free_numa(p, bytes, numa_node) */
+/* pinned + mapped host memory bound to NUMA node `numa_node` (1 GB-aligned mmap + mbind, registered in 1 GB
+ * pieces with retries; falls back to cudaHostAlloc; < 0: pm_host_alloc).  A single cudaMemcpy may not span two
+ * pieces: pm_copy_pieces / pm_copy_2d cut copies at 1 GB boundaries; the mapped device address
+ * (pm_host_device_ptr) covers the first piece.  Free with pm_host_free_numa(p, bytes, numa_node) */
 int pm_host_alloc_numa(unsigned long long bytes, int numa_node, void** out);
 int pm_host_free_numa(void* p, unsigned long long bytes, int numa_node);
 /* eager decode offload: host_dev + offs[2i] <- pool + offs[2i+1], `bytes` each, one kernel (`ctas` CTAs) writing
