@@ -1735,7 +1735,7 @@ extern "C" int pm_gemm_resid_rmsnorm(const void* w_packed, const void* tmap_x, i
   }
   const int post = (na.n_split > 0 && !(a.debug & 1) && !split_norm) ? POST_RESID_NORM : POST_NONE;
   rc = dispatch_bn(bn, [&](auto c) { return launch_any<decltype(c)::value>(cta_pair, tx, a, grid, st, post, &na); });
-  if (rc || post == POST_RESID_NORM || (a.debug & 16)) return rc;
+  if (rc || post == POST_RESID_NORM || (a.debug & (16 | 256))) return rc;   // 256: profiling, skip the norm
   return launch_rmsnorm(resid, norm_w, xn, m_tok, n_out, eps, st);
 }
 
