@@ -32,6 +32,9 @@ const char* pm_error_string(int code);
 int pm_tmap_encode_2d(void* tmap_out, const void* gaddr, unsigned long long inner, unsigned long long outer,
                       unsigned long long row_stride_bytes, unsigned box_inner, unsigned box_outer,
                       int swizzle128);
+/* 5-D map over the block-first KV pool (n_rows = blocks*16 slots of L_s*2*Hkv*hd bf16): one copy moves one KV
+ * block's K and V of one (layer, kv head); pm_paged_attention takes it with cfg bit 4 set */
+int pm_tmap_encode_pool(void* tmap_out, const void* pool, unsigned long long n_rows, int L_s, int Hkv, int hd);
 int pm_host_alloc(unsigned long long bytes, void** out);
 int pm_host_free(void* p);
 /* NUMA node of device `device`'s PCIe attachment (sysfs; -1 unknown) */
@@ -124,7 +127,9 @@ int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_tabl
                        int Hkv, int hd,
                        int layer, int L_s, int max_blocks, int max_chunks, int max_piece, int cfg,
                        void* stream);
-/* cfg: warps x KV-ring stages per SM (0: 6x4, 1: 12x2, 2: 8x3, 3: 4x2 at 2 CTAs/SM; -1: default);
+/* tmap_kv: the 2-D view [blocks*16][L_s*2*Hkv*hd] with a [16][64] box (pm_tmap_encode_2d, four copies
+ * per KV block), or -- cfg bit 4 (16) set -- pm_tmap_encode_pool's 5-D map (one copy per block).
+ * cfg & 15: warps x KV-ring stages per SM (0: 6x4, 1: 12x2, 2: 8x3, 3: 4x2 at 2 CTAs/SM; -1: default);
  * the work list must be built for pm_attn_workers_cfg(hd, cfg) warps and pieces of at most max_piece
  * (<= pm_attn_max_piece()) blocks; max_chunks >= the most pieces of one (row, kv head). */
 int pm_attn_max_piece(void);

@@ -19,6 +19,7 @@ _P, _I, _F, _U64, _LL = C.c_void_p, C.c_int, C.c_float, C.c_ulonglong, C.c_longl
 _SIGS = {
     "pm_abi_version": [],
     "pm_tmap_encode_2d": [_P, _P, _U64, _U64, _U64, C.c_uint, C.c_uint, _I],
+    "pm_tmap_encode_pool": [_P, _P, _U64, _I, _I, _I],
     "pm_host_alloc": [_U64, C.POINTER(_P)],
     "pm_host_free": [_P],
     "pm_device_numa_node": [_I, C.POINTER(_I)],

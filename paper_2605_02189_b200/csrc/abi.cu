@@ -52,6 +52,29 @@ extern "C" int pm_tmap_encode_2d(void* tmap_out, const void* gaddr, unsigned lon
   return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
 }
 
+// 5-D bf16 tensor map over the block-first KV pool [rows = block*16 + slot][L_s][k|v][Hkv][hd]
+// whose box is one KV block's K and V of one (layer, kv head) -- 16 slots x hd, both halves of
+// 64 dims, K and V -- in ONE copy: dims (innermost first) {64 dims, rows, hd/64 halves, k|v,
+// L_s*2*Hkv head columns}, byte strides {row pitch, 128, Hkv*hd*2, hd*2}, box {64, 16, hd/64,
+// 2, 1}, 128B swizzle.  The copy lands as [k|v][half][16 slots][128 B] -- the same shared
+// image the four 2-D boxes of pm_tmap_encode_2d produce -- at coordinates
+// (0, block*16, 0, 0, layer*2*Hkv + kv_head) (the k|v coordinate steps Hkv head columns).
+extern "C" int pm_tmap_encode_pool(void* tmap_out, const void* pool, unsigned long long n_rows, int L_s, int Hkv,
+                                   int hd) {
+  auto enc = get_encode();
+  if (!enc) return (int)cudaErrorNotSupported;
+  if (hd % 64 || L_s < 1 || Hkv < 1) return (int)cudaErrorInvalidValue;
+  const unsigned long long pitch = (unsigned long long)L_s * 2 * Hkv * hd * 2;
+  cuuint64_t dims[5] = {64, n_rows, (cuuint64_t)(hd / 64), 2, (cuuint64_t)L_s * 2 * Hkv};
+  cuuint64_t strides[4] = {pitch, 128, (cuuint64_t)Hkv * hd * 2, (cuuint64_t)hd * 2};
+  cuuint32_t box[5] = {64, 16, (cuuint32_t)(hd / 64), 2, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+                   const_cast<void*>(pool), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)cudaErrorInvalidValue;
+}
+
 // Pitched copy (cudaMemcpy2DAsync): `height` rows of `width` bytes, row
 // strides dpitch / spitch -- one layer's K/V of a run of tokens between the
 // pool and the host replica (token stride = the pitch).

@@ -82,6 +82,7 @@ struct AttnArgs {
   int M, H, Hkv, G, layer, max_blocks, max_chunks, maxp;
   float scale_log2;        // log2(e)/sqrt(hd)
   int debug;               // profiling only: bit0 skip the math (memory pipeline alone), bit2 trace
+  int kv5;                 // tmap is pm_tmap_encode_pool's 5-D map: one copy per KV block (else four 2-D boxes)
 };
 __device__ unsigned long long g_attn_trace[148 * 16 * 4];  // per warp: start, first data, end, blocks
 PM_DEV unsigned long long gtimer() {
@@ -223,10 +224,14 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
       const int col_v = ((a.layer * 2 + 1) * a.Hkv + pc.kvh) * HD;
       const uint64_t pol = policy_evict_first();
       mbar_arrive_expect_tx(&bars[s], 2 * C::TILE);
+      if (a.kv5) {   // [k|v][half][16 slots][128 B] in one copy
+        tma_load_5d(dst, &tmap_kv, &bars[s], 0, phys * 16, 0, 0, a.layer * 2 * a.Hkv + pc.kvh, pol);
+      } else {
 #pragma unroll
-      for (int hh = 0; hh < HALVES; ++hh) {
-        tma_load_2d(dst + hh * 2048, &tmap_kv, &bars[s], col_k + hh * 64, phys * 16, pol);
-        tma_load_2d(dst + C::TILE + hh * 2048, &tmap_kv, &bars[s], col_v + hh * 64, phys * 16, pol);
+        for (int hh = 0; hh < HALVES; ++hh) {
+          tma_load_2d(dst + hh * 2048, &tmap_kv, &bars[s], col_k + hh * 64, phys * 16, pol);
+          tma_load_2d(dst + C::TILE + hh * 2048, &tmap_kv, &bars[s], col_v + hh * 64, phys * 16, pol);
+        }
       }
       ++issued;
       if (++pc.blk == pc.nblk) p_live = item_setup(a, itm, pc.j + 1, nw, pc);
@@ -303,12 +308,22 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
     }
     const uint32_t pb0 = movmatrix_t(pack_bf16(p0, p1));  // tokens 0-7  -> b0
     const uint32_t pb1 = movmatrix_t(pack_bf16(p2, p3));  // tokens 8-15 -> b1
+    // A partial block's unwritten slots hold whatever the pool memory held
+    // (recycled allocations, prefetched host pages): P is 0 there, but 0 x Inf
+    // or 0 x NaN is NaN, so those V^T columns are zeroed (a0/a1 carry tokens
+    // 2t, 2t+1 and a2/a3 tokens 2t+8, 2t+9; the low half is the lower token).
+    uint32_t vm_lo = 0xffffffffu, vm_hi = 0xffffffffu;
+    if (tok0 + 16 > seq) {   // warp-uniform: the row's last block only
+      const int ta = tok0 + 2 * t, tb = ta + 8;
+      vm_lo = (ta < seq ? 0x0000ffffu : 0u) | (ta + 1 < seq ? 0xffff0000u : 0u);
+      vm_hi = (tb < seq ? 0x0000ffffu : 0u) | (tb + 1 < seq ? 0xffff0000u : 0u);
+    }
     // ---- O^T += V^T P^T
 #pragma unroll
     for (int mt = 0; mt < KC; ++mt) {
       uint32_t a0, a1, a2, a3;
       ldsm_x4_t(kbase + voff[mt], a0, a1, a2, a3);
-      mma16816(o[mt], a0, a1, a2, a3, pb0, pb1);
+      mma16816(o[mt], a0 & vm_lo, a1 & vm_lo, a2 & vm_hi, a3 & vm_hi, pb0, pb1);
     }
     __syncwarp();
     ++consumed;
@@ -518,7 +533,7 @@ int launch_attn(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st, int c
 }  // namespace
 
 // q [M][H][hd] bf16 (RoPE'd), pool via `tmap_kv` (2-D view [blocks*16][L_s*2*Hkv*hd],
-// box [16][64], 128B swizzle), block_table [M][max_blocks], seq_lens [M] (cached
+// box [16][64], 128B swizzle; or with cfg bit 4 set pm_tmap_encode_pool's 5-D map), block_table [M][max_blocks], seq_lens [M] (cached
 // positions incl. the current token), work = the step's balanced piece list
 // (pm_attn_work_list, built for pm_attn_workers_cfg(hd, cfg) warps and pieces of at
 // most `max_piece` blocks), out [M][H][hd] bf16.  ws_o/ws_ml hold
@@ -530,12 +545,14 @@ extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int*
                                   int max_chunks, int max_piece, int cfg, void* stream) {
   (void)L_s;
   if (M == 0) return 0;
+  const int kv5 = cfg >= 0 ? (cfg >> 4) & 1 : 0;   // bit 4: tmap_kv is pm_tmap_encode_pool's 5-D map
+  if (cfg >= 0) cfg &= 15;
   const int G = H / Hkv;
   if (H % Hkv || G > MAX_G || max_chunks < 1 || max_piece < 1 || max_piece > MAX_P || M > 65536 || Hkv > 65535)
     return (int)cudaErrorInvalidValue;
   AttnArgs a{reinterpret_cast<const bf16*>(q), block_table, seq_lens, reinterpret_cast<bf16*>(out),
              ws_o, ws_ml, counters, work, M, H, Hkv, G, layer, max_blocks, max_chunks, max_piece,
-             1.4426950408889634f / sqrtf((float)hd), attn_debug()};
+             1.4426950408889634f / sqrtf((float)hd), attn_debug(), kv5};
   auto tm = reinterpret_cast<const CUtensorMap*>(tmap_kv);
   auto st = reinterpret_cast<cudaStream_t>(stream);
   if (hd == 128) return launch_attn<128>(tm, a, st, cfg);

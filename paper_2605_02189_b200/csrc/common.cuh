@@ -75,6 +75,16 @@ PM_DEV void tma_load_2d(void* smem_dst, const void* tmap, uint64_t* bar, int x, 
         "r"(x), "r"(y), "l"(cache_policy)
       : "memory");
 }
+// 5-D tiled load global -> shared (coordinates innermost first).
+PM_DEV void tma_load_5d(void* smem_dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2, int c3, int c4,
+                        uint64_t cache_policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;"
+      ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "l"(cache_policy)
+      : "memory");
+}
 PM_DEV uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

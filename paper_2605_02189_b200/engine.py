@@ -199,9 +199,9 @@ class DecodeEngine:
             return
         if how == "none":   # caller fills the KV (prefill.run_prefill)
             return
-        # timing runs: random KV in HBM for resident blocks; the host replica
-        # keeps whatever the fresh pinned pages hold (zeros) -- values do not
-        # change the timing
+        # timing runs: random KV in HBM for resident blocks and in the host
+        # replica for the others (seeded: the replica's pinned pages may be
+        # recycled host memory, and two processes must hold the same values)
         for ex, kv in self.stages:
             # seeded per stage (its first layer), so a rank hosting one stage of a
             # pipeline holds the same KV as a process hosting all of them
@@ -210,6 +210,21 @@ class DecodeEngine:
             for rid, blocks in self.control.alloc.tables.items():
                 idx = torch.tensor(blocks, device=self.dev)
                 pv[idx] = (torch.randn(len(blocks), pv.shape[1], generator=gs, device=self.dev) * 0.5).to(torch.bfloat16)
+            bb = kv.block_bytes
+            for rid in rids:
+                if rid in self.control.alloc.tables:
+                    continue
+                nb = min(-(-self.requests[rid].prefix_len // 16), kv.rep.max_blocks)
+                if nb <= 0:
+                    continue
+                buf = (torch.randn(nb, bb // 2, generator=gs, device=self.dev) * 0.5).to(torch.bfloat16)
+                base = kv.rep.offset(self.slot_of[rid])
+                d = np.arange(nb, dtype=np.int64) * bb + base
+                s = np.arange(nb, dtype=np.int64) * bb
+                _C.call("pm_copy_pieces", _C.C.c_void_p(kv.rep.ptr), _C.C.c_void_p(buf.data_ptr()),
+                        d.ctypes.data_as(_C.C.c_void_p), s.ctypes.data_as(_C.C.c_void_p), nb, bb,
+                        _C.C.c_void_p(torch.cuda.current_stream().cuda_stream))
+                torch.cuda.current_stream().synchronize()
         torch.cuda.synchronize()
 
     def _prefill(self, prompts):

@@ -458,11 +458,29 @@ def qkv_rope_append(qkv, q_out, pool, block_table, positions, rope, qn_w, kn_w, 
             _stream(stream))
 
 
-def pool_tmap(pool: torch.Tensor, L_s: int, Hkv: int, hd: int) -> TensorMap:
-    """2-D TMA view of the block-first pool: rows = block*16 + slot, cols =
-    (layer, k|v, head, dim); box = 16 slots x 64 dims, 128B swizzle."""
+ATTN_KV5 = int(_os.environ.get("PM_ATTN_KV5", "0"))   # 5-D pool map: A/B measured neutral-to-slower at C2
+
+
+class PoolMap(TensorMap):
+    """pm_tmap_encode_pool's 5-D map of the block-first pool: one TMA copy
+    moves a KV block's K and V of one (layer, kv head)."""
+
+    def __init__(self, pool, n_rows, L_s, Hkv, hd):
+        self._raw = (C.c_ubyte * 192)()
+        self.addr = (C.addressof(self._raw) + 63) & ~63
+        self.tensor = pool
+        _C.call("pm_tmap_encode_pool", C.c_void_p(self.addr), C.c_void_p(pool.data_ptr()), n_rows, L_s, Hkv, hd)
+
+
+def pool_tmap(pool: torch.Tensor, L_s: int, Hkv: int, hd: int, kv5: bool = None) -> TensorMap:
+    """TMA map of the block-first pool for pm_paged_attention: the 2-D view
+    rows = block*16 + slot, cols = (layer, k|v, head, dim) with a 16 slots x 64
+    dims box, 128B swizzle (four copies per KV block; default), or the 5-D map
+    (one copy per block; ``kv5`` / PM_ATTN_KV5=1)."""
     n_rows = pool.numel() // (L_s * 2 * Hkv * hd)
     width = L_s * 2 * Hkv * hd
+    if ATTN_KV5 if kv5 is None else kv5:
+        return PoolMap(pool, n_rows, L_s, Hkv, hd)
     return TensorMap(pool, width, n_rows, width * 2, 64, 16)
 
 
@@ -606,10 +624,14 @@ def choose_attn_cfg(rows: int, hkv: int, hd: int, max_blocks: int) -> int:
 def paged_attention(tmap_kv, q, block_table, seq_lens, out, ws: AttnWorkspace, M, H, Hkv, hd, layer,
                     L_s, stream=None, kv_tokens=0):
     """``kv_tokens`` (sum of seq_lens, host-known) only feeds the optional timer."""
+    cfg = ws.cfg if ws.cfg >= 0 else int(_os.environ.get("PM_ATTN_CFG", "1"))
+    if isinstance(tmap_kv, PoolMap):
+        cfg |= 16   # the map kind travels with the call (bit 4)
+
     def go():
         _C.call("pm_paged_attention", tmap_kv.ptr, _ptr(q), _ptr(block_table), _ptr(seq_lens), _ptr(ws.work), _ptr(out),
                 _ptr(ws.o), _ptr(ws.ml), _ptr(ws.counters), M, H, Hkv, hd, layer, L_s, block_table.shape[1],
-                ws.max_chunks, ATTN_MAXP, ws.cfg, _stream(stream))
+                ws.max_chunks, ATTN_MAXP, cfg, _stream(stream))
     if TIMER is None:
         go()
     else:

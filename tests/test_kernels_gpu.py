@@ -107,11 +107,14 @@ def _pool(n_blocks, L_s, Hkv, hd):
     return torch.zeros(n_blocks * 16 * L_s * 2 * Hkv * hd, dtype=torch.bfloat16, device=DEV)
 
 
+@pytest.mark.parametrize("garbage,kv5", [(False, False), (True, False), (False, True), (True, True)])
 @pytest.mark.parametrize("spec", [TINY, QWEN3_8B, QWEN3_32B, LLAMA3_70B])   # GQA groups 2, 4, 8, 8
-def test_rope_append_and_paged_attention(spec):
+def test_rope_append_and_paged_attention(spec, garbage, kv5):
     """Random prefixes scattered over random physical blocks; the current
     token goes through the fused qk-norm/RoPE/append kernel, then attention
-    reads the whole prefix through the block table."""
+    reads the whole prefix through the block table.  garbage: every slot not
+    written holds NaN bits (a recycled pool allocation) -- the rows' partial
+    last blocks must not leak them into the output."""
     rng = np.random.default_rng(11)
     H, Hkv, hd, L_s, layer = spec.H, spec.Hkv, spec.hd, 3, 1
     lens = [1, 15, 16, 17, 100, 255, 256, 257, 700, 1025]  # prefix BEFORE this token
@@ -126,6 +129,8 @@ def test_rope_append_and_paged_attention(spec):
         tables[r, :nb] = perm[cur:cur + nb]
         cur += nb
     pool = _pool(n_blocks, L_s, Hkv, hd)
+    if garbage:
+        pool.view(torch.int16).fill_(-1)   # 0xffff: bf16 NaN
     P = pool.view(n_blocks, 16, L_s, 2, Hkv, hd)
     # existing prefix KV for positions < L (random, written through the table)
     hist_k = [rng.standard_normal((L, Hkv, hd)).astype(np.float32) for L in lens]
@@ -152,7 +157,7 @@ def test_rope_append_and_paged_attention(spec):
     aws = ops.AttnWorkspace(M, Hkv, hd, max_blocks, DEV)
     out = torch.empty(M, H, hd, dtype=torch.bfloat16, device=DEV)
     seq = pos + 1
-    tmap = ops.pool_tmap(pool, L_s, Hkv, hd)
+    tmap = ops.pool_tmap(pool, L_s, Hkv, hd, kv5=kv5)   # 2-D boxes or the 5-D one-copy map
     aws.set_work([L + 1 for L in lens])
     ops.paged_attention(tmap, q_out, bt, seq, out, aws, M, H, Hkv, hd, layer, L_s)
     torch.cuda.synchronize()
@@ -178,8 +183,10 @@ def test_rope_append_and_paged_attention(spec):
         want = ref.attend(q_out[r].float().cpu().numpy(), K, V, H // Hkv)
         got = out[r].float().cpu().numpy()
         np.testing.assert_allclose(got, want, atol=2e-2, rtol=2e-2, err_msg=f"row {r} len {L}")
-    # untouched layers / slots stay zero
-    assert np.all(Pn[:, :, 0] == 0) and np.all(Pn[:, :, 2] == 0)
+    assert np.isfinite(out.float().cpu().numpy()).all()
+    # untouched layers / slots stay as they were
+    if not garbage:
+        assert np.all(Pn[:, :, 0] == 0) and np.all(Pn[:, :, 2] == 0)
 
 
 @pytest.mark.parametrize("n_out,k,m", [(4096, 4096, 128), (512, 256, 7), (8192, 1024, 200), (512, 64, 16),
