@@ -530,7 +530,7 @@ def stage_summary(config, steps, warmup, peaks, local, calibrate=True):
            "decode_roofline_frac": r["decode_roofline"]["frac"],
            "t_hbm_ms": r["decode_roofline"]["t_hbm_ms"], "t_pcie_ms": r["decode_roofline"]["t_pcie_ms"],
            "kv_transfer_hidden_fraction": r["hidden"], "clocks": r["clocks"],
-           "estimator_fidelity": r["fidelity"]}
+           "estimator_fidelity": r["fidelity"], "online_refit": getattr(eng, "refit", None)}
     del eng
     free_engine()
     return out
@@ -596,6 +596,8 @@ def run_ours(args):
         est = {"planned_with": params_dict(eng.control.params), "analytic": params_dict(params),
                "step_fidelity": dev["fidelity"],
                "claim": "PAPER.md 667-669: >= 90% of steps within 5%, worst < 8%"}
+        if getattr(eng, "refit", None) is not None:   # warm-up periods -> delta shift (refit_online)
+            est["online_refit"] = eng.refit
         if eng.calibration is not None:
             est["max_rel_fit_err"] = eng.calibration["max_rel_fit_err"]
             est["samples"] = len(eng.calibration["samples"])

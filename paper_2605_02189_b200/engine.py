@@ -341,7 +341,7 @@ class DecodeEngine:
         torch.cuda.synchronize()
         return params
 
-    def refit_online(self, skip: int = 2):
+    def refit_online(self, skip: int = 1):
         """Closed loop on the running engine: the planner's predicted step time
         vs the measured step period of the steps run so far (CUDA events, this
         engine's lane mode and transfer load included) -> shift delta by the
@@ -351,12 +351,14 @@ class DecodeEngine:
         from .calibrate import step_errors
         torch.cuda.synchronize()
         pairs = step_errors(self.stages[0][1].records)[skip:]
-        if len(pairs) < 4:
+        if len(pairs) < 3:   # (the bench's 6 warm-up steps give 5 periods, 4 after the first)
+            self.refit = {"shift_s": 0.0, "periods": len(pairs)}
             return 0.0
         shift = float(np.median([meas - pred for pred, meas in pairs]))
         p = self.params
         self.params = EstimatorParams(p.alpha, p.beta, max(p.delta + shift, 1e-6))
         self.control.params = self.params
+        self.refit = {"shift_s": shift, "periods": len(pairs)}
         return shift
 
     def _hop_buffer(self, lane, resid):
