@@ -553,7 +553,7 @@ def run_ours(args):
                                                        calibrate=args.calibrate and world == 1)
     for _ in range(args.warmup):
         assert eng.step() is not None
-    if args.calibrate and world == 1:   # closed loop: the warm-up steps' measured periods correct the fit
+    if args.calibrate and args.refit and world == 1:   # closed loop: the warm-up steps' periods correct the fit
         eng.refit_online()
     torch.cuda.synchronize()
     dev = measure_device(eng, args.steps, peaks, local, dist)
@@ -681,6 +681,8 @@ def main():
     ap.add_argument("--no-calibrate", dest="calibrate", action="store_false",
                     help="plan with the analytic estimator instead of the on-box fit")
     ap.add_argument("--no-north-star", dest="north_star", action="store_false")
+    ap.add_argument("--no-refit", dest="refit", action="store_false",
+                    help="plan with the start-up grid fit only (no warm-up delta correction; A/B)")
     ap.add_argument("--config", default="c2", choices=["c2"] + sorted(STAGE_CONFIGS),
                     help="c2 (default): BASELINE configs[1] on one GPU; c3-*/c4-*: one PP=8 stage "
                          "(-last = the lm_head stage); c5-bs*-m*: one PP=4 stage of the C5 sweep")
