@@ -83,7 +83,6 @@ struct AttnArgs {
   float scale_log2;        // log2(e)/sqrt(hd)
   int debug;               // profiling only: bit0 skip the math (memory pipeline alone), bit2 trace
   int kv5;                 // tmap is pm_tmap_encode_pool's 5-D map: one copy per KV block (else four 2-D boxes)
-  int pf_dist;             // L2 prefetch of the block this many ahead of the ring's refill (0: off)
 };
 __device__ unsigned long long g_attn_trace[148 * 16 * 4];  // per warp: start, first data, end, blocks
 PM_DEV unsigned long long gtimer() {
@@ -237,29 +236,7 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
       ++issued;
       if (++pc.blk == pc.nblk) p_live = item_setup(a, itm, pc.j + 1, nw, pc);
     };
-    // L2 prefetch cursor (lane 0): pf_dist blocks beyond the ring, within this
-    // window's pieces -- more of the warp's KV in flight than its ring holds
-    Cursor fc = pc;
-    bool f_live = p_live && a.pf_dist > 0;
-    auto pf_one = [&]() {
-      if (!f_live) return;
-      const int phys = bid[fc.j * MAX_P + fc.blk];
-      if (a.kv5) {
-        tma_prefetch_5d(&tmap_kv, 0, phys * 16, 0, 0, a.layer * 2 * a.Hkv + fc.kvh);
-      } else {
-        const int ck = ((a.layer * 2 + 0) * a.Hkv + fc.kvh) * HD, cv = ck + a.Hkv * HD;
-#pragma unroll
-        for (int hh = 0; hh < HALVES; ++hh) {
-          tma_prefetch_2d(&tmap_kv, ck + hh * 64, phys * 16);
-          tma_prefetch_2d(&tmap_kv, cv + hh * 64, phys * 16);
-        }
-      }
-      if (++fc.blk == fc.nblk) f_live = item_setup(a, itm, fc.j + 1, nw, fc);
-    };
     if (lane == 0) {
-      for (int k = 0; k < STAGES && f_live; ++k)   // the ring's first blocks load directly
-        if (++fc.blk == fc.nblk) f_live = item_setup(a, itm, fc.j + 1, nw, fc);
-      for (int k = 0; k < a.pf_dist && f_live; ++k) pf_one();
       for (int k = 0; k < STAGES && p_live; ++k) issue_one();
     }
 
@@ -350,10 +327,7 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
     }
     __syncwarp();
     ++consumed;
-    if (lane == 0 && p_live) {  // refill the slot just consumed (reads done: __syncwarp)
-      issue_one();
-      pf_one();
-    }
+    if (lane == 0 && p_live) issue_one();  // refill the slot just consumed (reads done: __syncwarp)
     if (++cc.blk < cc.nblk) continue;
 
     // ---- item done: per-column row sums, then store or stash the partial
@@ -474,7 +448,6 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
 
 int num_sms();
 int attn_debug();
-int attn_pf_dist();
 
 template <int HD, int WARPS, int STAGES>
 int launch_cfg(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
@@ -505,13 +478,6 @@ int attn_cfg() {
     g_attn_cfg = e ? atoi(e) : 1;
   }
   return g_attn_cfg;
-}
-int attn_pf_dist() {   // PM_ATTN_PF: L2 prefetch distance in KV blocks (read once)
-  static const int v = [] {
-    const char* e = getenv("PM_ATTN_PF");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
 }
 int num_sms() {   // of the current device (cached per device)
   static int sms[64] = {0};
@@ -586,7 +552,7 @@ extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int*
     return (int)cudaErrorInvalidValue;
   AttnArgs a{reinterpret_cast<const bf16*>(q), block_table, seq_lens, reinterpret_cast<bf16*>(out),
              ws_o, ws_ml, counters, work, M, H, Hkv, G, layer, max_blocks, max_chunks, max_piece,
-             1.4426950408889634f / sqrtf((float)hd), attn_debug(), kv5, attn_pf_dist()};
+             1.4426950408889634f / sqrtf((float)hd), attn_debug(), kv5};
   auto tm = reinterpret_cast<const CUtensorMap*>(tmap_kv);
   auto st = reinterpret_cast<cudaStream_t>(stream);
   if (hd == 128) return launch_attn<128>(tm, a, st, cfg);

@@ -85,15 +85,6 @@ PM_DEV void tma_load_5d(void* smem_dst, const void* tmap, uint64_t* bar, int c0,
         "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "l"(cache_policy)
       : "memory");
 }
-// L2 prefetch of a 2-D / 5-D tensor box (no shared-memory destination, no completion).
-PM_DEV void tma_prefetch_2d(const void* tmap, int x, int y) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];"
-               ::"l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y) : "memory");
-}
-PM_DEV void tma_prefetch_5d(const void* tmap, int c0, int c1, int c2, int c3, int c4) {
-  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];"
-               ::"l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4) : "memory");
-}
 PM_DEV uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
