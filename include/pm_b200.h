@@ -129,6 +129,8 @@ int pm_paged_attention(const void* tmap_kv, const void* q, const int* block_tabl
                        void* stream);
 /* tmap_kv: the 2-D view [blocks*16][L_s*2*Hkv*hd] with a [16][64] box (pm_tmap_encode_2d, four copies
  * per KV block), or -- cfg bit 4 (16) set -- pm_tmap_encode_pool's 5-D map (one copy per block).
+ * cfg bit 5 (32): decode step -- every row is a distinct request whose only KV the preceding kernels write
+ * is its current token, so blocks before each row's last load ahead of the PDL dependency wait.
  * cfg & 15: warps x KV-ring stages per SM (0: 6x4, 1: 12x2, 2: 8x3, 3: 4x2 at 2 CTAs/SM; -1: default);
  * the work list must be built for pm_attn_workers_cfg(hd, cfg) warps and pieces of at most max_piece
  * (<= pm_attn_max_piece()) blocks; max_chunks >= the most pieces of one (row, kv head). */

@@ -83,6 +83,7 @@ struct AttnArgs {
   float scale_log2;        // log2(e)/sqrt(hd)
   int debug;               // profiling only: bit0 skip the math (memory pipeline alone), bit2 trace
   int kv5;                 // tmap is pm_tmap_encode_pool's 5-D map: one copy per KV block (else four 2-D boxes)
+  int early;               // decode step: KV blocks before a row's last may load before the dependency wait
 };
 __device__ unsigned long long g_attn_trace[148 * 16 * 4];  // per warp: start, first data, end, blocks
 PM_DEV unsigned long long gtimer() {
@@ -208,10 +209,6 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
       bid[idx] = k < nb ? __ldg(&a.block_table[(size_t)row * a.max_blocks + b0 + k]) : 0;
     }
     __syncwarp();
-    if (!waited) {
-      pdl_wait();  // q and the appended KV come from the previous kernel
-      waited = true;
-    }
 
     // producer cursor (lane 0 issues STAGES blocks ahead of the consumer)
     Cursor pc;
@@ -236,8 +233,22 @@ paged_attn_kernel(const __grid_constant__ CUtensorMap tmap_kv, AttnArgs a) {
       ++issued;
       if (++pc.blk == pc.nblk) p_live = item_setup(a, itm, pc.j + 1, nw, pc);
     };
+    int k0 = 0;
+    if (!waited) {
+      // Decode rows are distinct requests whose only KV the previous kernels
+      // write is the current token's (block (seq-1)/16 of its row, this
+      // layer): the ring's first blocks before that one are loaded ahead of
+      // the dependency wait, hiding the first-load latency behind the
+      // previous kernel's tail (a.early; not for prefill chunks, whose rows
+      // read each other's new tokens).
+      if (a.early && lane == 0)
+        for (; k0 < STAGES && p_live && pc.b0 + pc.blk < (pc.seq - 1) / 16; ++k0) issue_one();
+      __syncwarp();
+      pdl_wait();  // q and the appended KV come from the previous kernel
+      waited = true;
+    }
     if (lane == 0) {
-      for (int k = 0; k < STAGES && p_live; ++k) issue_one();
+      for (int k = k0; k < STAGES && p_live; ++k) issue_one();
     }
 
     Cursor cc, cn;
@@ -545,14 +556,15 @@ extern "C" int pm_paged_attention(const void* tmap_kv, const void* q, const int*
                                   int max_chunks, int max_piece, int cfg, void* stream) {
   (void)L_s;
   if (M == 0) return 0;
-  const int kv5 = cfg >= 0 ? (cfg >> 4) & 1 : 0;   // bit 4: tmap_kv is pm_tmap_encode_pool's 5-D map
+  const int kv5 = cfg >= 0 ? (cfg >> 4) & 1 : 0;     // bit 4: tmap_kv is pm_tmap_encode_pool's 5-D map
+  const int early = cfg >= 0 ? (cfg >> 5) & 1 : 0;   // bit 5: decode rows (early KV loads)
   if (cfg >= 0) cfg &= 15;
   const int G = H / Hkv;
   if (H % Hkv || G > MAX_G || max_chunks < 1 || max_piece < 1 || max_piece > MAX_P || M > 65536 || Hkv > 65535)
     return (int)cudaErrorInvalidValue;
   AttnArgs a{reinterpret_cast<const bf16*>(q), block_table, seq_lens, reinterpret_cast<bf16*>(out),
              ws_o, ws_ml, counters, work, M, H, Hkv, G, layer, max_blocks, max_chunks, max_piece,
-             1.4426950408889634f / sqrtf((float)hd), attn_debug(), kv5};
+             1.4426950408889634f / sqrtf((float)hd), attn_debug(), kv5, early};
   auto tm = reinterpret_cast<const CUtensorMap*>(tmap_kv);
   auto st = reinterpret_cast<cudaStream_t>(stream);
   if (hd == 128) return launch_attn<128>(tm, a, st, cfg);

@@ -621,12 +621,20 @@ def choose_attn_cfg(rows: int, hkv: int, hd: int, max_blocks: int) -> int:
     return 1 if rows >= ATTN_WIDE_ROWS else 2
 
 
+ATTN_EARLY = _os.environ.get("PM_ATTN_EARLY", "1") == "1"   # A/B switch
+
+
 def paged_attention(tmap_kv, q, block_table, seq_lens, out, ws: AttnWorkspace, M, H, Hkv, hd, layer,
-                    L_s, stream=None, kv_tokens=0):
-    """``kv_tokens`` (sum of seq_lens, host-known) only feeds the optional timer."""
+                    L_s, stream=None, kv_tokens=0, decode=False):
+    """``kv_tokens`` (sum of seq_lens, host-known) only feeds the optional timer.
+    ``decode``: every row is a different request whose only new KV is its
+    current token (not a prefill chunk), so the kernel may load the blocks
+    before each row's last ahead of its dependency wait (cfg bit 5)."""
     cfg = ws.cfg if ws.cfg >= 0 else int(_os.environ.get("PM_ATTN_CFG", "1"))
     if isinstance(tmap_kv, PoolMap):
         cfg |= 16   # the map kind travels with the call (bit 4)
+    if decode and ATTN_EARLY:
+        cfg |= 32
 
     def go():
         _C.call("pm_paged_attention", tmap_kv.ptr, _ptr(q), _ptr(block_table), _ptr(seq_lens), _ptr(ws.work), _ptr(out),

@@ -199,7 +199,8 @@ class StageExecutor:
             if layer_hook is not None:   # layer li's K/V is in the pool (prefill offload)
                 layer_hook(li)
             ops.paged_attention(self.pool_map, self.q, self.block_table, self.seq_lens, self.attn, self.aws,
-                                M, s.H, s.Hkv, s.hd, li, self.L_s, stream, kv_tokens=kv_tokens)
+                                M, s.H, s.Hkv, s.hd, li, self.L_s, stream, kv_tokens=kv_tokens,
+                                decode=not prefill_tokens)
             # O projection + residual + post-attention RMSNorm
             w["o"].resid_rmsnorm(self.attn_maps, M, self.resid, self.gws, w["mlp_norm"], self.xn, s.eps, stream,
                                  split_norm=self.split_norm, prefetch=pf(w["gu"]), site=4 * li + 1)

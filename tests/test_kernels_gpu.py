@@ -159,7 +159,9 @@ def test_rope_append_and_paged_attention(spec, garbage, kv5):
     seq = pos + 1
     tmap = ops.pool_tmap(pool, L_s, Hkv, hd, kv5=kv5)   # 2-D boxes or the 5-D one-copy map
     aws.set_work([L + 1 for L in lens])
-    ops.paged_attention(tmap, q_out, bt, seq, out, aws, M, H, Hkv, hd, layer, L_s)
+    # decode=garbage: the NaN-pool cases also load each row's older blocks ahead of the
+    # dependency wait on qkv_rope_append (cfg bit 5), the others after it
+    ops.paged_attention(tmap, q_out, bt, seq, out, aws, M, H, Hkv, hd, layer, L_s, decode=garbage)
     torch.cuda.synchronize()
     assert (aws.counters == 0).all()
     tab = rope_table(spec, 2048)
