@@ -15,6 +15,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none --csv --log-file $OUT/launches_c3.csv python bench.py --config c3-stage --steps 2 --warmup 3 --no-kernel-timing --no-cpu-baseline --no-calibrate > $OUT/ncu_c3.log 2>&1
 timeout 900 ncu --set full --import-source on --cache-control none --clock-control none -k regex:gemm_stream -s 400 -c 2 -o $OUT/gemm_full python bench.py --steps 2 --warmup 3 --no-kernel-timing --no-cpu-baseline --no-calibrate --no-north-star > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --cache-control none --clock-control none -k regex:paged_attn -s 100 -c 1 -o $OUT/attn_full python bench.py --steps 2 --warmup 3 --no-kernel-timing --no-cpu-baseline --no-calibrate --no-north-star > /dev/null 2>&1
-STEPS=30 bash tools/c5_sweep.sh
-python tools/c5_table.py gpurun_out/c5 > $OUT/c5_table.md 2>&1
+if [ -z "${SKIP_C5:-}" ]; then
+  STEPS=30 bash tools/c5_sweep.sh
+  python tools/c5_table.py gpurun_out/c5 > $OUT/c5_table.md 2>&1
+fi
 ls -la $OUT
