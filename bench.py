@@ -282,6 +282,47 @@ def build_engine(config, rank=0, world=1, local=0, calibrate=True):
 _PCIE = {}
 
 
+_HBM = {}
+
+
+def hbm_probe(local=0):
+    """Device-to-device copy rate (read + write bytes / s) of a 2 GB buffer
+    in this process (best of 3): a diagnostic of the run's HBM state, not the
+    roofline peak (MEASURED_PEAKS.json)."""
+    import torch
+    if local not in _HBM:
+        n = 2 << 30
+        a = torch.empty(n, dtype=torch.uint8, device=f"cuda:{local}")
+        b = torch.empty_like(a)
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            b.copy_(a)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, 2 * n / (e0.elapsed_time(e1) * 1e-3))
+        _HBM[local] = best
+        del a, b
+    return _HBM[local]
+
+
+def host_placement(local=0):
+    """CPU and NUMA node the bench process runs on vs the GPU's node."""
+    out = {}
+    try:
+        cpu = int(open("/proc/self/stat").read().rsplit(")", 1)[1].split()[36])
+        out["cpu"] = cpu
+        nodes = [d for d in os.listdir(f"/sys/devices/system/cpu/cpu{cpu}") if d.startswith("node")]
+        out["cpu_node"] = int(nodes[0][4:]) if nodes else None
+        out["allowed_cpus"] = len(os.sched_getaffinity(0))
+        from paper_2605_02189_b200.kv import device_numa_node
+        out["gpu_node"] = device_numa_node(local)
+    except Exception as e:   # diagnostic only
+        out["error"] = repr(e)
+    return out
+
+
 def pcie_peak(local=0):
     """(H2D, D2H) bytes/s of a 256 MB pinned <-> device copy on this box
     (best of 3, CUDA events; measured once per process)."""
@@ -370,6 +411,7 @@ def measure_device(eng, steps, peaks, local=0, dist=None):
                             "roofline_tok_s": roof_tok_s, "frac": value / roof_tok_s,
                             "peak_hbm_gbs": peaks["hbm_gbs"],
                             "pcie_peak_GBps": {"h2d": pk_h2d / 1e9, "d2h": pk_d2h / 1e9},
+                            "hbm_probe_GBps": hbm_probe(local) / 1e9, "host": host_placement(local),
                             "note": "per step: weights once + the active micro-batch's KV + new KV + activations "
                                     "over HBM (measured peak) vs prefetch / offload bytes over the PCIe link "
                                     "(a 256 MB pinned copy per direction on this box)"},
